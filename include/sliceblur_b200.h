@@ -1,0 +1,119 @@
+/*
+ * sliceblur_b200.h - C ABI of the B200 (sm_100a) running-sum Gaussian filter.
+ *
+ * This is the drop-in boundary for the reference package `sliceblur`
+ * (/root/reference/pkg/src/sliceblur/).  The reference is pure Python/numpy
+ * and has no FFI of its own; each entry point below replaces one function of
+ * its filtering module, and the host package `paper_1107_4958_b200` binds them
+ * with ctypes (see INTEGRATION.md for the binding a sliceblur maintainer would
+ * add).
+ *
+ *   sb_check_kernel          <- filtering.py:39-45   _check_kernel
+ *   sb_separable_filter_2d   <- filtering.py:76-104  separable_filter_2d
+ *                               (+ batched / interleaved-channel layouts that
+ *                               the reference reaches by looping in Python)
+ *   sb_slice_filter_1d       <- filtering.py:67-73   slice_filter_1d
+ *   sb_prefix_sum_f64        <- filtering.py:31-36   prefix_sum
+ *   sb_filter_rows           <- filtering.py:48-64   _filter_rows (row pass only)
+ *
+ * Conventions
+ *   - All image/signal pointers are DEVICE pointers owned by the caller; the
+ *     library never allocates or frees memory and keeps no global mutable
+ *     state besides a thread-local error string (sb_last_error).
+ *   - Strides are in ELEMENTS.  `channels` > 1 means interleaved channels
+ *     (pixel stride = channels); every channel is filtered independently.
+ *   - Work is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream) and is stream-ordered: the call returns before
+ *     the GPU finishes.
+ *   - `radii` (int64, strictly increasing, >= 0) and `weights` (float64) are
+ *     exactly the SliceKernel arrays of the reference (approx.py:82-129).
+ *   - Arithmetic: exact int32 fixed-point running sums.  For
+ *     uint8/uint16 input the first pass is exact; float input is quantised
+ *     with a quantum derived from `value_bound` (an upper bound on |pixel|;
+ *     pass <= 0 to declare "unknown", which the host wrapper resolves with a
+ *     device max before calling).  Pixels violating the bound are reported
+ *     through `status_dev` (bit SB_STATUS_RANGE) - never silently.
+ *   - Return value: SB_OK or an error code; the message is in sb_last_error().
+ */
+#ifndef SLICEBLUR_B200_H
+#define SLICEBLUR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SB_MAX_K 8
+
+/* return codes */
+enum {
+  SB_OK = 0,
+  SB_ERR_INVALID_ARGUMENT = 1, /* -> ValueError (filtering.py:34-35, 70-71, 85-86)          */
+  SB_ERR_KERNEL_TOO_LARGE = 2, /* -> KernelTooLargeError (filtering.py:27-28, 40-43)          */
+  SB_ERR_NOT_UNIT_DC = 3,      /* -> ValueError "kernel must have unit DC gain" (44-45)       */
+  SB_ERR_CUDA = 4,             /* launch / runtime failure                                    */
+  SB_ERR_WORKSPACE = 5         /* workspace pointer NULL or smaller than sb_*_workspace_bytes */
+};
+
+/* source element types */
+enum { SB_DTYPE_U8 = 0, SB_DTYPE_U16 = 1, SB_DTYPE_F32 = 2, SB_DTYPE_F64 = 3 };
+
+/* bits written (atomicOr) into *status_dev by the kernels */
+#define SB_STATUS_RANGE 1 /* a pixel exceeded value_bound (or was NaN/Inf) */
+
+/* ABI version, bumped on any signature change. */
+int sb_version(void);
+
+/* Thread-local description of the last error returned on this thread. */
+const char* sb_last_error(void);
+
+/* filtering.py:39-45: SB_ERR_KERNEL_TOO_LARGE if radii[k-1] >= extent,
+ * SB_ERR_NOT_UNIT_DC if |sum w_i (2 p_i + 1) - 1| > 1e-6, else SB_OK. */
+int sb_check_kernel(const int64_t* radii, const double* weights, int k, int64_t extent);
+
+/* Bytes of device workspace sb_separable_filter_2d needs for this shape
+ * (0 when the single fused kernel applies; the size of the int32
+ * intermediate when the radius needs the two-kernel path). */
+size_t sb_separable_filter_2d_workspace_bytes(int64_t batch, int64_t height, int64_t width, int channels,
+                                              const int64_t* radii, int k);
+
+/* filtering.py:76-104 separable_filter_2d over a batch of images:
+ *   dst[b, y, x, c] = cols(rows(src[b, :, :, c]))[y, x]
+ * src: `batch` images of `height` x `width` pixels with `channels`
+ * interleaved channels, element type `src_dtype`; dst: float32, same
+ * layout rules.  src_image_stride / dst_image_stride may be 0 when batch == 1.
+ * Validates like the reference: height/width >= 1, kernel fits both extents
+ * (KernelTooLarge), unit DC gain. */
+int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_t height, int64_t width,
+                           int channels, int64_t src_image_stride, int64_t src_row_stride, float* dst,
+                           int64_t dst_image_stride, int64_t dst_row_stride, const int64_t* radii,
+                           const double* weights, int k, double value_bound, void* workspace,
+                           size_t workspace_bytes, int* status_dev, void* stream);
+
+/* filtering.py:48-64 _filter_rows: the row pass alone, every row of a
+ * (rows x width) array (row stride in elements), float32 output. */
+int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, int64_t src_row_stride,
+                   float* dst, int64_t dst_row_stride, const int64_t* radii, const double* weights, int k,
+                   double value_bound, int* status_dev, void* stream);
+
+/* filtering.py:67-73 slice_filter_1d on one signal of length n. */
+int sb_slice_filter_1d(const void* src, int src_dtype, int64_t n, float* dst, const int64_t* radii,
+                       const double* weights, int k, double value_bound, int* status_dev, void* stream);
+
+/* filtering.py:31-36 prefix_sum: inclusive float64 scan of n >= 1 values.
+ * Needs sb_prefix_sum_workspace_bytes(n) bytes of device workspace. */
+size_t sb_prefix_sum_workspace_bytes(int64_t n);
+int sb_prefix_sum_f64(const double* src, double* dst, int64_t n, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
+/* max |x| over n elements of a device array (float32/float64/u8/u16),
+ * written as a double to *out_dev; used by the host wrapper to derive
+ * value_bound when the caller does not supply one. */
+int sb_max_abs(const void* src, int src_dtype, int64_t n, double* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLICEBLUR_B200_H */

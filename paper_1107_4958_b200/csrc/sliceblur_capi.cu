@@ -1,0 +1,349 @@
+// sliceblur_capi.cu - C ABI (include/sliceblur_b200.h) over the sm_100a sweep kernels.
+//
+// Host-side responsibilities, mirroring the reference where it validates
+// (filtering.py:39-45, 67-73, 76-104): argument checks, the fixed-point quanta
+// (DESIGN.md "Arithmetic"), the choice between the fused single-launch sweep
+// and the two-launch path, and the work decomposition over 148 SMs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "sliceblur_b200.h"
+#include "sweep_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kHB = 16;        // rows per band (must match sweep_kernel)
+constexpr int kStripW = 128;   // columns per CTA
+constexpr size_t kSmemBudget = 200 * 1024;
+
+int validate_kernel(const int64_t* radii, const double* weights, int k) {
+  if (!radii || !weights) return fail(SB_ERR_INVALID_ARGUMENT, "radii/weights must not be NULL");
+  if (k < 1 || k > SB_MAX_K)
+    return fail(SB_ERR_INVALID_ARGUMENT, "need 1 <= k <= " + std::to_string(SB_MAX_K) + " slices");
+  if (radii[0] < 0) return fail(SB_ERR_INVALID_ARGUMENT, "slice radii must be strictly increasing and >= 0");
+  for (int i = 1; i < k; ++i)
+    if (radii[i] <= radii[i - 1])
+      return fail(SB_ERR_INVALID_ARGUMENT, "slice radii must be strictly increasing and >= 0");
+  for (int i = 0; i < k; ++i)
+    if (!std::isfinite(weights[i])) return fail(SB_ERR_INVALID_ARGUMENT, "slice weights must be finite");
+  return SB_OK;
+}
+
+// Largest s with bound * 2^s < limit (strict), clamped to a sane exponent range.
+int quantum_exponent(double bound, double limit) {
+  if (!(bound > 0.0)) return 0;
+  int s = (int)std::floor(std::log2(limit / bound));
+  while (s > -120 && std::ldexp(bound, s) >= limit) --s;
+  while (s < 100 && std::ldexp(bound, s + 1) < limit) ++s;
+  return std::max(-120, std::min(100, s));
+}
+
+struct Plan {
+  sb::Taps taps;
+  int pmax;
+};
+
+int make_taps(const int64_t* radii, const double* weights, int k, int src_dtype, double value_bound, Plan* plan) {
+  int rc = validate_kernel(radii, weights, k);
+  if (rc) return rc;
+  double bound;
+  switch (src_dtype) {
+    case SB_DTYPE_U8: bound = 255.0; break;
+    case SB_DTYPE_U16: bound = 65535.0; break;
+    case SB_DTYPE_F32:
+    case SB_DTYPE_F64:
+      if (!(value_bound >= 0.0) || !std::isfinite(value_bound))
+        return fail(SB_ERR_INVALID_ARGUMENT, "float input needs a finite value_bound >= 0 (max |pixel|)");
+      bound = value_bound;
+      break;
+    default: return fail(SB_ERR_INVALID_ARGUMENT, "unknown src_dtype");
+  }
+  const int pmax = (int)radii[k - 1];
+  const double width = 2.0 * pmax + 1.0;
+  const double box_limit = 2147483647.0 - 2.0 * width;  // |box sum| < 2^31 incl. rounding
+  int s_in = 0;
+  if (src_dtype == SB_DTYPE_F32 || src_dtype == SB_DTYPE_F64) {
+    s_in = std::min(quantum_exponent(bound, 4194304.0), quantum_exponent(width * bound, box_limit));
+  } else if (width * bound >= box_limit) {
+    return fail(SB_ERR_INVALID_ARGUMENT, "radius too large for exact int32 box sums of this dtype");
+  }
+  double gabs = 0.0;
+  for (int i = 0; i < k; ++i) gabs += std::fabs(weights[i]) * (2.0 * radii[i] + 1.0);
+  // |R| <= gabs * (bound + half an input quantum)
+  const double rbound = gabs * (bound + std::ldexp(0.5, -s_in)) * (1.0 + 1e-6);
+  const int s_mid = std::min(quantum_exponent(rbound, 4194304.0), quantum_exponent(width * rbound, box_limit));
+
+  sb::Taps& t = plan->taps;
+  std::memset(&t, 0, sizeof(t));
+  t.k = k;
+  t.pmax = pmax;
+  for (int i = 0; i < k; ++i) {
+    t.p[i] = (int)radii[i];
+    t.w_row[i] = (float)std::ldexp(weights[i], s_mid - s_in);
+    t.w_col[i] = (float)std::ldexp(weights[i], -s_mid);
+    t.w_out1[i] = (float)std::ldexp(weights[i], -s_in);
+  }
+  t.in_scale = (float)std::ldexp(1.0, s_in);
+  t.in_limit = 4194304.0f;
+  plan->pmax = pmax;
+  return SB_OK;
+}
+
+int dtype_size(int dt) {
+  switch (dt) {
+    case SB_DTYPE_U8: return 1;
+    case SB_DTYPE_U16: return 2;
+    case SB_DTYPE_F32: return 4;
+    case SB_DTYPE_F64: return 8;
+  }
+  return 0;
+}
+
+struct Launch {
+  sb::Tiling tl;
+  size_t smem;
+  dim3 grid;
+};
+
+size_t stage_bytes(int L) { return (size_t)kHB * L * sizeof(int); }
+size_t ring_bytes(int D, int Ws) { return (size_t)2 * D * Ws * sizeof(int); }
+
+bool fused_fits(int pmax) {
+  int L = (kStripW + 2 * pmax + 1 + 3) & ~3;
+  int D = kHB + 2 * pmax + 1;
+  return stage_bytes(L) + ring_bytes(D, kStripW) <= kSmemBudget;
+}
+
+template <typename Tin, int K, sb::Mode M>
+const void* kernel_ptr() {
+  return (const void*)sb::sweep_kernel<Tin, K, M>;
+}
+
+template <typename Tin, sb::Mode M>
+const void* kernel_for_k(int k) {
+  switch (k) {
+    case 1: return kernel_ptr<Tin, 1, M>();
+    case 2: return kernel_ptr<Tin, 2, M>();
+    case 3: return kernel_ptr<Tin, 3, M>();
+    case 4: return kernel_ptr<Tin, 4, M>();
+    case 5: return kernel_ptr<Tin, 5, M>();
+    case 6: return kernel_ptr<Tin, 6, M>();
+    case 7: return kernel_ptr<Tin, 7, M>();
+    default: return kernel_ptr<Tin, 8, M>();
+  }
+}
+
+template <sb::Mode M>
+const void* kernel_for(int dtype, int k) {
+  switch (dtype) {
+    case SB_DTYPE_U8: return kernel_for_k<uint8_t, M>(k);
+    case SB_DTYPE_U16: return kernel_for_k<uint16_t, M>(k);
+    case SB_DTYPE_F32: return kernel_for_k<float, M>(k);
+    default: return kernel_for_k<double, M>(k);
+  }
+}
+
+const void* pick_kernel(sb::Mode m, int dtype, int k) {
+  switch (m) {
+    case sb::Mode::Fused: return kernel_for<sb::Mode::Fused>(dtype, k);
+    case sb::Mode::RowsToMid: return kernel_for<sb::Mode::RowsToMid>(dtype, k);
+    case sb::Mode::RowsToOut: return kernel_for<sb::Mode::RowsToOut>(dtype, k);
+    default: return kernel_for<sb::Mode::ColsFromMid>(SB_DTYPE_U8, k);  // source unused
+  }
+}
+
+// Work decomposition: every (strip, channel) column sweeps `items` contiguous
+// row ranges of the tall (batch*H) image; items is sized so the grid fills the
+// GPU about once, but never so small that the 2*pmax+1 warm-up rows of a
+// column sweep exceed ~1/8 of the rows it outputs.
+int plan_launch(const void* fn, sb::Mode m, int pmax, int W, long long total_rows, int channels, Launch* out) {
+  sb::Tiling& tl = out->tl;
+  tl.Ws = kStripW;
+  tl.L = (kStripW + 2 * pmax + 1 + 3) & ~3;
+  tl.D = kHB + 2 * pmax + 1;
+  tl.nstrips = (W + kStripW - 1) / kStripW;
+  size_t smem = 0;
+  if (m != sb::Mode::ColsFromMid) smem += stage_bytes(tl.L);
+  if (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid) smem += ring_bytes(tl.D, kStripW);
+  out->smem = smem;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kStripW, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  occ = std::max(occ, 1);
+  const long long slots = (long long)sms * occ;
+  const long long columns = (long long)tl.nstrips * channels;
+  long long items = std::max(1LL, slots / columns);
+  const bool sweeps = (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid);
+  const long long min_rows = sweeps ? 8LL * (2 * pmax + 1) : kHB;
+  items = std::min(items, std::max(1LL, total_rows / min_rows));
+  long long rows_per_item = (total_rows + items - 1) / items;
+  if (!sweeps) rows_per_item = ((rows_per_item + kHB - 1) / kHB) * kHB;
+  items = (total_rows + rows_per_item - 1) / rows_per_item;
+  tl.rows_per_item = rows_per_item;
+  if (columns * items > 0x7fffffffLL) return fail(SB_ERR_INVALID_ARGUMENT, "image too large for the grid");
+  out->grid = dim3((unsigned)(tl.nstrips * items), (unsigned)channels, 1);
+  return SB_OK;
+}
+
+int launch(const void* fn, const Launch& L, const void* src, const int* mid_in, int* mid_out, float* dst,
+           const sb::Geometry& g, const sb::Taps& t, int* status, cudaStream_t stream) {
+  void* args[] = {(void*)&src, (void*)&mid_in, (void*)&mid_out, (void*)&dst,
+                  (void*)&g,   (void*)&t,      (void*)&L.tl,    (void*)&status};
+  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(kStripW), args, L.smem, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+  return SB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sb_version(void) { return 1; }
+
+const char* sb_last_error(void) { return g_last_error.c_str(); }
+
+int sb_check_kernel(const int64_t* radii, const double* weights, int k, int64_t extent) {
+  int rc = validate_kernel(radii, weights, k);
+  if (rc) return rc;
+  if (radii[k - 1] >= extent)
+    return fail(SB_ERR_KERNEL_TOO_LARGE, "slice radius " + std::to_string(radii[k - 1]) + " does not fit extent " +
+                                             std::to_string(extent));
+  double dc = 0.0;
+  for (int i = 0; i < k; ++i) dc += weights[i] * (2.0 * (double)radii[i] + 1.0);
+  if (std::fabs(dc - 1.0) > 1e-6) return fail(SB_ERR_NOT_UNIT_DC, "kernel must have unit DC gain; call normalized()");
+  return SB_OK;
+}
+
+size_t sb_separable_filter_2d_workspace_bytes(int64_t batch, int64_t height, int64_t width, int channels,
+                                              const int64_t* radii, int k) {
+  if (!radii || k < 1 || k > SB_MAX_K || batch < 1 || height < 1 || width < 1 || channels < 1) return 0;
+  if (fused_fits((int)radii[k - 1])) return 0;
+  return (size_t)batch * height * width * channels * sizeof(int);
+}
+
+int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_t height, int64_t width,
+                           int channels, int64_t src_image_stride, int64_t src_row_stride, float* dst,
+                           int64_t dst_image_stride, int64_t dst_row_stride, const int64_t* radii,
+                           const double* weights, int k, double value_bound, void* workspace,
+                           size_t workspace_bytes, int* status_dev, void* stream) {
+  if (!src || !dst) return fail(SB_ERR_INVALID_ARGUMENT, "src/dst must not be NULL");
+  if (batch < 1 || height < 1 || width < 1) return fail(SB_ERR_INVALID_ARGUMENT, "need a non-empty 2D image");
+  if (channels < 1) return fail(SB_ERR_INVALID_ARGUMENT, "channels must be >= 1");
+  if (height > 0x7fffffff || width > 0x7fffffff) return fail(SB_ERR_INVALID_ARGUMENT, "extent exceeds int32");
+  if (src_row_stride < width * channels || dst_row_stride < width * channels)
+    return fail(SB_ERR_INVALID_ARGUMENT, "row stride smaller than width * channels");
+  if (batch > 1 && (src_image_stride < height * src_row_stride || dst_image_stride < height * dst_row_stride))
+    return fail(SB_ERR_INVALID_ARGUMENT, "image stride smaller than height * row stride");
+  int rc = sb_check_kernel(radii, weights, k, width);
+  if (rc) return rc;
+  rc = sb_check_kernel(radii, weights, k, height);
+  if (rc) return rc;
+  Plan plan;
+  rc = make_taps(radii, weights, k, src_dtype, value_bound, &plan);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+
+  sb::Geometry g;
+  g.in_img = src_image_stride;
+  g.in_row = src_row_stride;
+  g.in_px = channels;
+  g.out_img = dst_image_stride;
+  g.out_row = dst_row_stride;
+  g.out_px = channels;
+  g.H = (int)height;
+  g.W = (int)width;
+  g.nimg = (int)batch;
+  const long long total_rows = (long long)batch * height;
+
+  if (fused_fits(plan.pmax)) {
+    g.mid_img = g.mid_row = 0;
+    const void* fn = pick_kernel(sb::Mode::Fused, src_dtype, k);
+    Launch L;
+    rc = plan_launch(fn, sb::Mode::Fused, plan.pmax, g.W, total_rows, channels, &L);
+    if (rc) return rc;
+    return launch(fn, L, src, nullptr, nullptr, dst, g, plan.taps, status_dev, st);
+  }
+  // two launches through an int32 workspace laid out [channel][batch][H][W]
+  const size_t need = sb_separable_filter_2d_workspace_bytes(batch, height, width, channels, radii, k);
+  if (!workspace || workspace_bytes < need)
+    return fail(SB_ERR_WORKSPACE, "workspace of " + std::to_string(need) + " bytes required");
+  int* mid = (int*)workspace;
+  g.mid_row = width;
+  g.mid_img = (long long)height * width;
+  const long long mid_channel = g.mid_img * batch;
+  // RowsToMid / ColsFromMid index the workspace per channel through blockIdx.y;
+  // keep the channel planes separate by launching per channel.
+  for (int ch = 0; ch < channels; ++ch) {
+    const char* src_c = (const char*)src + (size_t)ch * dtype_size(src_dtype);
+    const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);
+    Launch L1;
+    rc = plan_launch(f1, sb::Mode::RowsToMid, plan.pmax, g.W, total_rows, 1, &L1);
+    if (rc) return rc;
+    rc = launch(f1, L1, src_c, nullptr, mid + ch * mid_channel, nullptr, g, plan.taps, status_dev, st);
+    if (rc) return rc;
+    const void* f2 = pick_kernel(sb::Mode::ColsFromMid, src_dtype, k);
+    Launch L2;
+    rc = plan_launch(f2, sb::Mode::ColsFromMid, plan.pmax, g.W, total_rows, 1, &L2);
+    if (rc) return rc;
+    rc = launch(f2, L2, nullptr, mid + ch * mid_channel, nullptr, dst + ch, g, plan.taps, status_dev, st);
+    if (rc) return rc;
+  }
+  return SB_OK;
+}
+
+int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, int64_t src_row_stride, float* dst,
+                   int64_t dst_row_stride, const int64_t* radii, const double* weights, int k, double value_bound,
+                   int* status_dev, void* stream) {
+  if (!src || !dst) return fail(SB_ERR_INVALID_ARGUMENT, "src/dst must not be NULL");
+  if (rows < 1 || width < 1) return fail(SB_ERR_INVALID_ARGUMENT, "need a non-empty signal");
+  if (rows > 0x7fffffff || width > 0x7fffffff) return fail(SB_ERR_INVALID_ARGUMENT, "extent exceeds int32");
+  if (src_row_stride < width || dst_row_stride < width)
+    return fail(SB_ERR_INVALID_ARGUMENT, "row stride smaller than width");
+  int rc = sb_check_kernel(radii, weights, k, width);
+  if (rc) return rc;
+  Plan plan;
+  rc = make_taps(radii, weights, k, src_dtype, value_bound, &plan);
+  if (rc) return rc;
+  sb::Geometry g;
+  std::memset(&g, 0, sizeof(g));
+  g.in_row = src_row_stride;
+  g.in_px = 1;
+  g.out_row = dst_row_stride;
+  g.out_px = 1;
+  g.H = (int)rows;
+  g.W = (int)width;
+  g.nimg = 1;
+  const void* fn = pick_kernel(sb::Mode::RowsToOut, src_dtype, k);
+  Launch L;
+  rc = plan_launch(fn, sb::Mode::RowsToOut, plan.pmax, g.W, rows, 1, &L);
+  if (rc) return rc;
+  return launch(fn, L, src, nullptr, nullptr, dst, g, plan.taps, status_dev, (cudaStream_t)stream);
+}
+
+int sb_slice_filter_1d(const void* src, int src_dtype, int64_t n, float* dst, const int64_t* radii,
+                       const double* weights, int k, double value_bound, int* status_dev, void* stream) {
+  if (n < 1) return fail(SB_ERR_INVALID_ARGUMENT, "need a non-empty 1D signal");
+  return sb_filter_rows(src, src_dtype, 1, n, n, dst, n, radii, weights, k, value_bound, status_dev, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,286 @@
+"""Drop-in GPU replacement of the reference filtering module.
+
+Mirrors ``/root/reference/pkg/src/sliceblur/filtering.py``: same function
+names, argument meaning and exceptions (``ValueError`` for bad shapes,
+``KernelTooLargeError`` when a slice radius reaches an extent, ``ValueError``
+for a non-unit-DC kernel).  Every call runs the sm_100a kernels of
+``libsliceblur_b200.so`` through its C ABI; there is no CPU path.
+
+Differences from the reference, by design:
+
+* results are float32 (the reference returns float64); they agree with the
+  reference within max-abs 1e-3 on a 0-255 scale (tests/test_gpu_parity.py);
+* inputs may be numpy arrays (copied to the GPU and back) or CUDA
+  ``torch.Tensor`` objects (filtered in place on the device, result returned
+  as a CUDA tensor);
+* float inputs are quantised to int32 fixed point with a quantum derived from
+  ``value_bound`` (max |pixel|).  When it is not given, it is measured on the
+  device.  A pixel above the bound raises ``ValueError``, never a wrong answer.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+from .approx import SliceKernel
+
+__all__ = [
+    "KernelTooLargeError",
+    "filter_rows",
+    "prefix_sum",
+    "separable_filter_2d",
+    "separable_filter_batch",
+    "slice_filter_1d",
+]
+
+_DC_TOL = 1e-6
+
+
+class KernelTooLargeError(ValueError):
+    """A slice radius reaches or exceeds the filtered extent (filtering.py:27-28)."""
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+_DTYPE_CODES = {
+    np.dtype(np.uint8): nat.SB_DTYPE_U8,
+    np.dtype(np.uint16): nat.SB_DTYPE_U16,
+    np.dtype(np.float32): nat.SB_DTYPE_F32,
+    np.dtype(np.float64): nat.SB_DTYPE_F64,
+}
+
+
+def _kernel_arrays(kernel: SliceKernel):
+    radii = np.ascontiguousarray(kernel.radii, dtype=np.int64)
+    weights = np.ascontiguousarray(kernel.weights, dtype=np.float64)
+    return (
+        radii,
+        weights,
+        radii.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        weights.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+    )
+
+
+def _raise_for(code: int):
+    if code == nat.SB_OK:
+        return
+    msg = nat.last_error()
+    if code == nat.SB_ERR_KERNEL_TOO_LARGE:
+        raise KernelTooLargeError(msg)
+    if code in (nat.SB_ERR_INVALID_ARGUMENT, nat.SB_ERR_NOT_UNIT_DC):
+        raise ValueError(msg)
+    raise RuntimeError(f"sliceblur_b200 error {code}: {msg}")
+
+
+def _check_kernel(kernel: SliceKernel, n: int):
+    """Mirror of filtering.py:39-45 (also enforced again inside the C ABI)."""
+    if kernel.max_radius >= n:
+        raise KernelTooLargeError(f"slice radius {kernel.max_radius} does not fit extent {n}")
+    if abs(kernel.dc_gain - 1.0) > _DC_TOL:
+        raise ValueError("kernel must have unit DC gain; call normalized()")
+    if kernel.k > nat.SB_MAX_K:
+        raise ValueError(f"at most {nat.SB_MAX_K} slices are supported on the GPU path")
+
+
+class _Device:
+    """Moves an input to the GPU (if needed) and remembers how to return the result."""
+
+    def __init__(self, data):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("sliceblur_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+        nat.load()
+        self.torch = torch
+        self.host_tensor = False
+        if isinstance(data, torch.Tensor):
+            self.from_numpy = False
+            if data.is_cuda:
+                t = data
+            else:
+                # host tensor (pinned for speed): H2D on the current stream
+                self.host_tensor = True
+                t = data.to(device="cuda", non_blocking=data.is_pinned())
+        else:
+            self.from_numpy = True
+            arr = np.asarray(data)
+            if arr.dtype not in _DTYPE_CODES:
+                # the reference converts everything to float64 (filtering.py:84)
+                arr = arr.astype(np.float64)
+            t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+        codes = {torch.uint8: nat.SB_DTYPE_U8, torch.float32: nat.SB_DTYPE_F32, torch.float64: nat.SB_DTYPE_F64}
+        if hasattr(torch, "uint16"):
+            codes[torch.uint16] = nat.SB_DTYPE_U16
+        if t.dtype not in codes:
+            t = t.to(torch.float64)
+        self.tensor = t.contiguous()
+        self.code = codes[self.tensor.dtype]
+        self.stream = torch.cuda.current_stream().cuda_stream
+
+    def value_bound(self, given):
+        if self.code in (nat.SB_DTYPE_U8, nat.SB_DTYPE_U16):
+            return 0.0  # exact integer path; bound implied by the dtype
+        if given is not None:
+            return float(given)
+        out = self.torch.zeros(1, dtype=self.torch.float64, device=self.tensor.device)
+        _raise_for(nat.load().sb_max_abs(self.tensor.data_ptr(), self.code, self.tensor.numel(), out.data_ptr(),
+                                          self.stream))
+        bound = float(out.item())
+        if not np.isfinite(bound):
+            raise ValueError("input contains NaN or Inf; the fixed-point GPU path needs finite pixels")
+        return bound
+
+    def finish(self, result, status, check: bool, host_out=None):
+        if check and int(status.item()) & nat.SB_STATUS_RANGE:
+            raise ValueError("a pixel exceeds value_bound (or is not finite)")
+        if host_out is not None:
+            host_out.copy_(result.view(host_out.shape))
+            return host_out
+        if self.from_numpy:
+            return result.cpu().numpy()
+        if self.host_tensor:
+            return result.cpu()
+        return result
+
+
+def separable_filter_batch(images, kernel: SliceKernel, *, channels_last: bool = False, value_bound=None,
+                           out=None, check: bool = True):
+    """Filter a batch of images: (B, H, W) or, with ``channels_last``,
+    (B, H, W, C) / (H, W, C) with interleaved channels each filtered separately.
+
+    The per-image arithmetic is ``separable_filter_2d``'s (filtering.py:76-104).
+    Returns float32 of the input's shape (numpy in -> numpy out, CUDA tensor in
+    -> CUDA tensor out, host tensor in -> host tensor out).  ``out`` may supply a
+    preallocated contiguous float32 tensor: on the GPU it is written in place,
+    on the host (ideally pinned) the result is copied into it.
+    """
+    dev = _Device(images)
+    x = dev.tensor
+    if channels_last:
+        if x.dim() == 3:
+            x = x.unsqueeze(0)
+        if x.dim() != 4:
+            raise ValueError("channels_last input must be (H, W, C) or (B, H, W, C)")
+        b, h, w, c = x.shape
+    else:
+        if x.dim() == 2:
+            x = x.unsqueeze(0)
+        if x.dim() != 3:
+            raise ValueError("need a (B, H, W) batch of 2D images")
+        b, h, w = x.shape
+        c = 1
+    if min(b, h, w, c) < 1:
+        raise ValueError("need a non-empty 2D image")
+    _check_kernel(kernel, w)
+    _check_kernel(kernel, h)
+    torch = dev.torch
+    host_out = None
+    if out is not None:
+        if out.dtype != torch.float32 or not out.is_contiguous() or out.numel() != x.numel():
+            raise ValueError("out must be a contiguous float32 tensor of the input's size")
+        if out.is_cuda:
+            result = out
+        else:
+            host_out = out  # D2H into the caller's (pinned) host buffer
+            result = torch.empty(tuple(dev.tensor.shape), dtype=torch.float32, device=x.device)
+    else:
+        result = torch.empty(tuple(dev.tensor.shape), dtype=torch.float32, device=x.device)
+    radii, weights, rp, wp = _kernel_arrays(kernel)
+    lib = nat.load()
+    ws_bytes = lib.sb_separable_filter_2d_workspace_bytes(b, h, w, c, rp, kernel.k)
+    workspace = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=x.device)
+    status = torch.zeros(1, dtype=torch.int32, device=x.device)
+    bound = dev.value_bound(value_bound)
+    code = lib.sb_separable_filter_2d(
+        x.data_ptr(), dev.code, b, h, w, c, h * w * c, w * c,
+        result.data_ptr(), h * w * c, w * c,
+        rp, wp, kernel.k, bound,
+        workspace.data_ptr(), int(ws_bytes), status.data_ptr(), dev.stream,
+    )
+    _raise_for(code)
+    return dev.finish(result, status, check, host_out)
+
+
+def separable_filter_2d(image, kernel: SliceKernel, parallel: bool = False, *, value_bound=None, out=None,
+                        check: bool = True):
+    """Rows then columns, replicate boundary (filtering.py:76-104), on the GPU.
+
+    ``parallel`` is accepted for signature compatibility and ignored (the GPU
+    path is always parallel; the reference's results are identical either way).
+    """
+    del parallel
+    if isinstance(image, np.ndarray) or not hasattr(image, "dim"):
+        arr = np.asarray(image)
+        if arr.ndim != 2:
+            raise ValueError("need a 2D image")
+    elif image.dim() != 2:
+        raise ValueError("need a 2D image")
+    return separable_filter_batch(image, kernel, value_bound=value_bound, out=out, check=check)
+
+
+def filter_rows(arr, kernel: SliceKernel, *, value_bound=None, check: bool = True):
+    """The row pass alone on every row of a 2D array (filtering.py:48-64)."""
+    dev = _Device(arr)
+    x = dev.tensor
+    if x.dim() != 2 or x.shape[0] < 1 or x.shape[1] < 1:
+        raise ValueError("need a non-empty 2D array")
+    m, n = x.shape
+    _check_kernel(kernel, n)
+    torch = dev.torch
+    result = torch.empty((m, n), dtype=torch.float32, device=x.device)
+    radii, weights, rp, wp = _kernel_arrays(kernel)
+    status = torch.zeros(1, dtype=torch.int32, device=x.device)
+    bound = dev.value_bound(value_bound)
+    _raise_for(nat.load().sb_filter_rows(x.data_ptr(), dev.code, m, n, n, result.data_ptr(), n, rp, wp, kernel.k,
+                                         bound, status.data_ptr(), dev.stream))
+    return dev.finish(result, status, check)
+
+
+def slice_filter_1d(signal, kernel: SliceKernel, *, value_bound=None, check: bool = True):
+    """Filter a 1D signal with a unit-gain slice kernel (filtering.py:67-73)."""
+    dev = _Device(signal)
+    x = dev.tensor
+    if x.dim() != 1 or x.numel() < 1:
+        raise ValueError("need a non-empty 1D signal")
+    n = x.numel()
+    _check_kernel(kernel, n)
+    torch = dev.torch
+    result = torch.empty(n, dtype=torch.float32, device=x.device)
+    radii, weights, rp, wp = _kernel_arrays(kernel)
+    status = torch.zeros(1, dtype=torch.int32, device=x.device)
+    bound = dev.value_bound(value_bound)
+    _raise_for(nat.load().sb_slice_filter_1d(x.data_ptr(), dev.code, n, result.data_ptr(), rp, wp, kernel.k, bound,
+                                             status.data_ptr(), dev.stream))
+    return dev.finish(result, status, check)
+
+
+def prefix_sum(values):
+    """Inclusive float64 cumulative sum (filtering.py:31-36) on the GPU."""
+    torch = _torch()
+    if isinstance(values, torch.Tensor):
+        t = values.to(device="cuda", dtype=torch.float64).contiguous()
+        from_numpy = False
+    else:
+        arr = np.asarray(values, dtype=np.float64)
+        if arr.ndim != 1 or arr.size < 1:
+            raise ValueError("need a non-empty 1D signal")
+        if not torch.cuda.is_available():
+            raise RuntimeError("sliceblur_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+        t = torch.from_numpy(arr).cuda()
+        from_numpy = True
+    if t.dim() != 1 or t.numel() < 1:
+        raise ValueError("need a non-empty 1D signal")
+    lib = nat.load()
+    n = t.numel()
+    ws = int(lib.sb_prefix_sum_workspace_bytes(n))
+    workspace = torch.empty(max(ws, 8), dtype=torch.uint8, device=t.device)
+    out = torch.empty_like(t)
+    _raise_for(lib.sb_prefix_sum_f64(t.data_ptr(), out.data_ptr(), n, workspace.data_ptr(), ws,
+                                     torch.cuda.current_stream().cuda_stream))
+    return out.cpu().numpy() if from_numpy else out

@@ -1,0 +1,97 @@
+"""The C-ABI library loads here (no GPU) and exports everything the header declares.
+
+Only host-side entry points are called: argument validation returns before any
+CUDA call, so these run on the CPU-only build container.
+"""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1107_4958_b200 import _native as nat
+from paper_1107_4958_b200 import approx as A
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    text = open(os.path.join(ROOT, "include", "sliceblur_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sb_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(nat.LIB_PATH):
+        from paper_1107_4958_b200 import build
+
+        build.build()
+    return nat.load()
+
+
+def test_exports_every_header_symbol(lib):
+    syms = _header_symbols()
+    assert set(syms) == set(nat.EXPORTED_SYMBOLS)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert lib.sb_version() == 1
+
+
+def _k(radii, weights):
+    r = np.ascontiguousarray(radii, np.int64)
+    w = np.ascontiguousarray(weights, np.float64)
+    return r, w, r.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def test_check_kernel_mirrors_reference(lib):
+    kern = A.table_kernel(3, 20.0)  # max radius 47
+    r, w, rp, wp = _k(kern.radii, kern.weights)
+    assert lib.sb_check_kernel(rp, wp, kern.k, 200) == nat.SB_OK
+    assert lib.sb_check_kernel(rp, wp, kern.k, 47) == nat.SB_ERR_KERNEL_TOO_LARGE
+    assert "does not fit extent 47" in nat.last_error()
+    assert lib.sb_check_kernel(rp, wp, kern.k, 48) == nat.SB_OK
+    r2, w2, rp2, wp2 = _k([2], [1.0])
+    assert lib.sb_check_kernel(rp2, wp2, 1, 30) == nat.SB_ERR_NOT_UNIT_DC
+    r3, w3, rp3, wp3 = _k([3, 3], [0.1, 0.1])
+    assert lib.sb_check_kernel(rp3, wp3, 2, 30) == nat.SB_ERR_INVALID_ARGUMENT
+    r4, w4, rp4, wp4 = _k(list(range(9)), [1.0 / 81] * 9)
+    assert lib.sb_check_kernel(rp4, wp4, 9, 100) == nat.SB_ERR_INVALID_ARGUMENT
+
+
+def test_invalid_arguments_fail_before_cuda(lib):
+    kern = A.table_kernel(3, 5.0)
+    r, w, rp, wp = _k(kern.radii, kern.weights)
+    f = lib.sb_separable_filter_2d
+    # NULL src
+    assert f(None, nat.SB_DTYPE_F32, 1, 64, 64, 1, 0, 64, 1, 0, 64, rp, wp, 3, 255.0, None, 0, None, None) == \
+        nat.SB_ERR_INVALID_ARGUMENT
+    # empty image
+    assert f(1, nat.SB_DTYPE_F32, 1, 0, 64, 1, 0, 64, 1, 0, 64, rp, wp, 3, 255.0, None, 0, None, None) == \
+        nat.SB_ERR_INVALID_ARGUMENT
+    # kernel too large in either dimension (filtering.py:88-89)
+    assert f(1, nat.SB_DTYPE_F32, 1, 11, 64, 1, 0, 64, 1, 0, 64, rp, wp, 3, 255.0, None, 0, None, None) == \
+        nat.SB_ERR_KERNEL_TOO_LARGE
+    assert f(1, nat.SB_DTYPE_F32, 1, 64, 11, 1, 0, 11, 1, 0, 11, rp, wp, 3, 255.0, None, 0, None, None) == \
+        nat.SB_ERR_KERNEL_TOO_LARGE
+    # float input without a bound
+    assert f(1, nat.SB_DTYPE_F32, 1, 64, 64, 1, 0, 64, 1, 0, 64, rp, wp, 3, -1.0, None, 0, None, None) == \
+        nat.SB_ERR_INVALID_ARGUMENT
+    # stride too small
+    assert f(1, nat.SB_DTYPE_U8, 1, 64, 64, 3, 0, 64, 1, 0, 192, rp, wp, 3, 0.0, None, 0, None, None) == \
+        nat.SB_ERR_INVALID_ARGUMENT
+    assert lib.sb_slice_filter_1d(1, nat.SB_DTYPE_F32, 0, 1, rp, wp, 3, 1.0, None, None) == nat.SB_ERR_INVALID_ARGUMENT
+    assert lib.sb_prefix_sum_f64(None, None, 0, None, 0, None) == nat.SB_ERR_INVALID_ARGUMENT
+
+
+def test_workspace_sizes(lib):
+    small = A.table_kernel(3, 10.0)  # pmax 23 -> fused, no workspace
+    r, w, rp, wp = _k(small.radii, small.weights)
+    assert lib.sb_separable_filter_2d_workspace_bytes(256, 1024, 1024, 1, rp, 3) == 0
+    big = A.table_kernel(4, 100.0)  # pmax 257 -> two launches through an int32 plane
+    r, w, rp, wp = _k(big.radii, big.weights)
+    assert lib.sb_separable_filter_2d_workspace_bytes(1, 1000, 2000, 3, rp, 4) == 1000 * 2000 * 3 * 4
+    assert lib.sb_prefix_sum_workspace_bytes(1) == 8
+    assert lib.sb_prefix_sum_workspace_bytes(2048 * 3 + 1) == 4 * 8
