@@ -28,9 +28,9 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(SB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-constexpr int kHB = 16;        // rows per band (must match sweep_kernel)
-constexpr int kStripW = 128;   // columns per CTA
 constexpr size_t kSmemBudget = 200 * 1024;
+
+int ceil16(int v) { return (v + 15) & ~15; }
 
 int validate_kernel(const int64_t* radii, const double* weights, int k) {
   if (!radii || !weights) return fail(SB_ERR_INVALID_ARGUMENT, "radii/weights must not be NULL");
@@ -121,13 +121,33 @@ struct Launch {
   dim3 grid;
 };
 
-size_t stage_bytes(int L) { return (size_t)kHB * L * sizeof(int); }
-size_t ring_bytes(int D, int Ws) { return (size_t)2 * D * Ws * sizeof(int); }
+// Tiling of a strip sweep (see sweep_kernels.cuh): staged/prefix row [xb, xb+L)
+// with xb = x0 - xoff, ring of D + HB rows for the fused mode.
+sb::Tiling make_tiling(int pmax, int channels, int es, bool u8_single) {
+  sb::Tiling tl;
+  std::memset(&tl, 0, sizeof(tl));
+  tl.xoff = ceil16(pmax + 1);
+  tl.L = ceil16(tl.xoff + sb::WS + pmax);
+  const int nchunk = tl.L / sb::CH;
+  int lpr = 1;
+  while (lpr < nchunk && lpr < 32) lpr <<= 1;
+  tl.lanes_per_row = lpr;
+  tl.stage_row_bytes = ceil16(tl.L * channels * es);
+  tl.D = 2 * pmax + 2 * sb::HB;
+  tl.packed = (u8_single && (2 * pmax + 1) * 255 < 32768 && nchunk <= 32) ? 1 : 0;
+  return tl;
+}
 
-bool fused_fits(int pmax) {
-  int L = (kStripW + 2 * pmax + 1 + 3) & ~3;
-  int D = kHB + 2 * pmax + 1;
-  return stage_bytes(L) + ring_bytes(D, kStripW) <= kSmemBudget;
+size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
+  if (m == sb::Mode::ColsFromMid) return 0;
+  size_t s = (size_t)2 * sb::HB * tl.stage_row_bytes + (size_t)sb::HB * tl.L * sizeof(int);
+  if (m == sb::Mode::Fused) s += (size_t)(tl.D + sb::HB) * sb::WS * sizeof(int);
+  return s;
+}
+
+bool fused_fits(int pmax, int channels, int es) {
+  sb::Tiling tl = make_tiling(pmax, channels, es, false);
+  return smem_bytes(tl, sb::Mode::Fused) <= kSmemBudget;
 }
 
 template <typename Tin, int K, sb::Mode M>
@@ -172,32 +192,30 @@ const void* pick_kernel(sb::Mode m, int dtype, int k) {
 // row ranges of the tall (batch*H) image; items is sized so the grid fills the
 // GPU about once, but never so small that the 2*pmax+1 warm-up rows of a
 // column sweep exceed ~1/8 of the rows it outputs.
-int plan_launch(const void* fn, sb::Mode m, int pmax, int W, long long total_rows, int channels, Launch* out) {
+int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int W, long long total_rows, int channels,
+                Launch* out) {
   sb::Tiling& tl = out->tl;
-  tl.Ws = kStripW;
-  tl.L = (kStripW + 2 * pmax + 1 + 3) & ~3;
-  tl.D = kHB + 2 * pmax + 1;
-  tl.nstrips = (W + kStripW - 1) / kStripW;
-  size_t smem = 0;
-  if (m != sb::Mode::ColsFromMid) smem += stage_bytes(tl.L);
-  if (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid) smem += ring_bytes(tl.D, kStripW);
+  tl = base;
+  tl.nstrips = (W + sb::WS - 1) / sb::WS;
+  const int pmax = (tl.D - 2 * sb::HB) / 2;
+  const size_t smem = smem_bytes(tl, m);
   out->smem = smem;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kStripW, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, sb::WS, smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
   occ = std::max(occ, 1);
   const long long slots = (long long)sms * occ;
   const long long columns = (long long)tl.nstrips * channels;
   long long items = std::max(1LL, slots / columns);
   const bool sweeps = (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid);
-  const long long min_rows = sweeps ? 8LL * (2 * pmax + 1) : kHB;
+  const long long min_rows = sweeps ? 8LL * (2 * pmax + 1) : sb::HB;
   items = std::min(items, std::max(1LL, total_rows / min_rows));
   long long rows_per_item = (total_rows + items - 1) / items;
-  if (!sweeps) rows_per_item = ((rows_per_item + kHB - 1) / kHB) * kHB;
+  if (!sweeps) rows_per_item = ((rows_per_item + sb::HB - 1) / sb::HB) * sb::HB;
   items = (total_rows + rows_per_item - 1) / rows_per_item;
   tl.rows_per_item = rows_per_item;
   if (columns * items > 0x7fffffffLL) return fail(SB_ERR_INVALID_ARGUMENT, "image too large for the grid");
@@ -209,7 +227,7 @@ int launch(const void* fn, const Launch& L, const void* src, const int* mid_in, 
            const sb::Geometry& g, const sb::Taps& t, int* status, cudaStream_t stream) {
   void* args[] = {(void*)&src, (void*)&mid_in, (void*)&mid_out, (void*)&dst,
                   (void*)&g,   (void*)&t,      (void*)&L.tl,    (void*)&status};
-  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(kStripW), args, L.smem, stream);
+  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::WS), args, L.smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   return SB_OK;
 }
@@ -237,7 +255,8 @@ int sb_check_kernel(const int64_t* radii, const double* weights, int k, int64_t 
 size_t sb_separable_filter_2d_workspace_bytes(int64_t batch, int64_t height, int64_t width, int channels,
                                               const int64_t* radii, int k) {
   if (!radii || k < 1 || k > SB_MAX_K || batch < 1 || height < 1 || width < 1 || channels < 1) return 0;
-  if (fused_fits((int)radii[k - 1])) return 0;
+  // the dtype only changes the staged bytes; decide with the widest common one (f32)
+  if (fused_fits((int)radii[k - 1], channels, 4)) return 0;
   return (size_t)batch * height * width * channels * sizeof(int);
 }
 
@@ -264,51 +283,51 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
   cudaStream_t st = (cudaStream_t)stream;
 
   sb::Geometry g;
+  std::memset(&g, 0, sizeof(g));
   g.in_img = src_image_stride;
   g.in_row = src_row_stride;
   g.in_px = channels;
+  g.es = dtype_size(src_dtype);
   g.out_img = dst_image_stride;
   g.out_row = dst_row_stride;
   g.out_px = channels;
   g.H = (int)height;
   g.W = (int)width;
   g.nimg = (int)batch;
+  g.aligned16 = ((uintptr_t)src % 16 == 0) && ((src_row_stride * g.es) % 16 == 0) &&
+                (batch == 1 || (src_image_stride * g.es) % 16 == 0);
   const long long total_rows = (long long)batch * height;
+  const bool u8_single = (src_dtype == SB_DTYPE_U8 && channels == 1);
+  const sb::Tiling base = make_tiling(plan.pmax, channels, g.es, u8_single);
 
-  if (fused_fits(plan.pmax)) {
-    g.mid_img = g.mid_row = 0;
+  const size_t need = sb_separable_filter_2d_workspace_bytes(batch, height, width, channels, radii, k);
+  if (need == 0) {
     const void* fn = pick_kernel(sb::Mode::Fused, src_dtype, k);
     Launch L;
-    rc = plan_launch(fn, sb::Mode::Fused, plan.pmax, g.W, total_rows, channels, &L);
+    rc = plan_launch(fn, sb::Mode::Fused, base, g.W, total_rows, channels, &L);
     if (rc) return rc;
     return launch(fn, L, src, nullptr, nullptr, dst, g, plan.taps, status_dev, st);
   }
   // two launches through an int32 workspace laid out [channel][batch][H][W]
-  const size_t need = sb_separable_filter_2d_workspace_bytes(batch, height, width, channels, radii, k);
   if (!workspace || workspace_bytes < need)
     return fail(SB_ERR_WORKSPACE, "workspace of " + std::to_string(need) + " bytes required");
   int* mid = (int*)workspace;
   g.mid_row = width;
   g.mid_img = (long long)height * width;
-  const long long mid_channel = g.mid_img * batch;
-  // RowsToMid / ColsFromMid index the workspace per channel through blockIdx.y;
-  // keep the channel planes separate by launching per channel.
-  for (int ch = 0; ch < channels; ++ch) {
-    const char* src_c = (const char*)src + (size_t)ch * dtype_size(src_dtype);
-    const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);
-    Launch L1;
-    rc = plan_launch(f1, sb::Mode::RowsToMid, plan.pmax, g.W, total_rows, 1, &L1);
-    if (rc) return rc;
-    rc = launch(f1, L1, src_c, nullptr, mid + ch * mid_channel, nullptr, g, plan.taps, status_dev, st);
-    if (rc) return rc;
-    const void* f2 = pick_kernel(sb::Mode::ColsFromMid, src_dtype, k);
-    Launch L2;
-    rc = plan_launch(f2, sb::Mode::ColsFromMid, plan.pmax, g.W, total_rows, 1, &L2);
-    if (rc) return rc;
-    rc = launch(f2, L2, nullptr, mid + ch * mid_channel, nullptr, dst + ch, g, plan.taps, status_dev, st);
-    if (rc) return rc;
-  }
-  return SB_OK;
+  g.mid_ch = g.mid_img * batch;
+  const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);
+  Launch L1;
+  sb::Tiling rows_tiling = base;
+  rows_tiling.packed = 0;
+  rc = plan_launch(f1, sb::Mode::RowsToMid, rows_tiling, g.W, total_rows, channels, &L1);
+  if (rc) return rc;
+  rc = launch(f1, L1, src, nullptr, mid, nullptr, g, plan.taps, status_dev, st);
+  if (rc) return rc;
+  const void* f2 = pick_kernel(sb::Mode::ColsFromMid, src_dtype, k);
+  Launch L2;
+  rc = plan_launch(f2, sb::Mode::ColsFromMid, base, g.W, total_rows, channels, &L2);
+  if (rc) return rc;
+  return launch(f2, L2, nullptr, mid, nullptr, dst, g, plan.taps, status_dev, st);
 }
 
 int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, int64_t src_row_stride, float* dst,
@@ -328,14 +347,16 @@ int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, 
   std::memset(&g, 0, sizeof(g));
   g.in_row = src_row_stride;
   g.in_px = 1;
+  g.es = dtype_size(src_dtype);
   g.out_row = dst_row_stride;
   g.out_px = 1;
   g.H = (int)rows;
   g.W = (int)width;
   g.nimg = 1;
+  g.aligned16 = ((uintptr_t)src % 16 == 0) && ((src_row_stride * g.es) % 16 == 0);
   const void* fn = pick_kernel(sb::Mode::RowsToOut, src_dtype, k);
   Launch L;
-  rc = plan_launch(fn, sb::Mode::RowsToOut, plan.pmax, g.W, rows, 1, &L);
+  rc = plan_launch(fn, sb::Mode::RowsToOut, make_tiling(plan.pmax, 1, g.es, false), g.W, rows, 1, &L);
   if (rc) return rc;
   return launch(fn, L, src, nullptr, nullptr, dst, g, plan.taps, status_dev, (cudaStream_t)stream);
 }
