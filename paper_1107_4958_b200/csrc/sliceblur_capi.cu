@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -133,58 +134,41 @@ sb::Tiling make_tiling(int pmax, int channels, int es, bool u8_single) {
   while (lpr < nchunk && lpr < 32) lpr <<= 1;
   tl.lanes_per_row = lpr;
   tl.stage_row_bytes = ceil16(tl.L * channels * es);
-  tl.D = 2 * pmax + 2 * sb::HB;
-  tl.packed = (u8_single && (2 * pmax + 1) * 255 < 32768 && nchunk <= 32) ? 1 : 0;
+  tl.ls = tl.L <= sb::LS ? sb::LS : tl.L;  // the fused kernel is compiled for stride LS
+  tl.D = ((2 * pmax + 2 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;  // multiple of HB
+  tl.packed = (u8_single && (2 * pmax + 1) * 255 < 32768 && nchunk <= 32 && tl.L <= sb::LSP) ? 1 : 0;
+  int cols = 32;
+  while (cols < tl.D + sb::HB) cols <<= 1;
+  tl.tmem_cols = cols;
   return tl;
 }
 
 size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
   if (m == sb::Mode::ColsFromMid) return 0;
-  size_t s = (size_t)2 * sb::HB * tl.stage_row_bytes + (size_t)sb::HB * tl.L * sizeof(int);
-  if (m == sb::Mode::Fused) s += (size_t)(tl.D + sb::HB) * sb::WS * sizeof(int);
+  const size_t prefix = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP * sizeof(int) : (size_t)sb::HB * tl.ls * sizeof(int);
+  size_t s = (size_t)2 * sb::HB * tl.stage_row_bytes + prefix;
+  if (m == sb::Mode::Fused) {
+    // the ring lives in tensor memory: cap residency at 512 / tmem_cols CTAs per SM by
+    // asking for enough shared memory, so no CTA ever waits inside tcgen05.alloc
+    const int ctas = 512 / tl.tmem_cols;
+    const size_t floor_bytes = 233472 / (size_t)(ctas + 1) - 1024 + 16;
+    s = std::max(s, floor_bytes);
+  }
   return s;
 }
 
 bool fused_fits(int pmax, int channels, int es) {
   sb::Tiling tl = make_tiling(pmax, channels, es, false);
-  return smem_bytes(tl, sb::Mode::Fused) <= kSmemBudget;
-}
-
-template <typename Tin, int K, sb::Mode M>
-const void* kernel_ptr() {
-  return (const void*)sb::sweep_kernel<Tin, K, M>;
-}
-
-template <typename Tin, sb::Mode M>
-const void* kernel_for_k(int k) {
-  switch (k) {
-    case 1: return kernel_ptr<Tin, 1, M>();
-    case 2: return kernel_ptr<Tin, 2, M>();
-    case 3: return kernel_ptr<Tin, 3, M>();
-    case 4: return kernel_ptr<Tin, 4, M>();
-    case 5: return kernel_ptr<Tin, 5, M>();
-    case 6: return kernel_ptr<Tin, 6, M>();
-    case 7: return kernel_ptr<Tin, 7, M>();
-    default: return kernel_ptr<Tin, 8, M>();
-  }
-}
-
-template <sb::Mode M>
-const void* kernel_for(int dtype, int k) {
-  switch (dtype) {
-    case SB_DTYPE_U8: return kernel_for_k<uint8_t, M>(k);
-    case SB_DTYPE_U16: return kernel_for_k<uint16_t, M>(k);
-    case SB_DTYPE_F32: return kernel_for_k<float, M>(k);
-    default: return kernel_for_k<double, M>(k);
-  }
+  return tl.L <= sb::LS && tl.tmem_cols <= 512 && smem_bytes(tl, sb::Mode::Fused) <= kSmemBudget;
 }
 
 const void* pick_kernel(sb::Mode m, int dtype, int k) {
-  switch (m) {
-    case sb::Mode::Fused: return kernel_for<sb::Mode::Fused>(dtype, k);
-    case sb::Mode::RowsToMid: return kernel_for<sb::Mode::RowsToMid>(dtype, k);
-    case sb::Mode::RowsToOut: return kernel_for<sb::Mode::RowsToOut>(dtype, k);
-    default: return kernel_for<sb::Mode::ColsFromMid>(SB_DTYPE_U8, k);  // source unused
+  if (m == sb::Mode::ColsFromMid) return sb::sweep_ptr_cols(k);  // source unused
+  switch (dtype) {
+    case SB_DTYPE_U8: return sb::sweep_ptr_u8(m, k);
+    case SB_DTYPE_U16: return sb::sweep_ptr_u16(m, k);
+    case SB_DTYPE_F32: return sb::sweep_ptr_f32(m, k);
+    default: return sb::sweep_ptr_f64(m, k);
   }
 }
 
@@ -192,21 +176,33 @@ const void* pick_kernel(sb::Mode m, int dtype, int k) {
 // row ranges of the tall (batch*H) image; items is sized so the grid fills the
 // GPU about once, but never so small that the 2*pmax+1 warm-up rows of a
 // column sweep exceed ~1/8 of the rows it outputs.
-int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int W, long long total_rows, int channels,
-                Launch* out) {
+int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, int W, long long total_rows,
+                int channels, Launch* out) {
   sb::Tiling& tl = out->tl;
   tl = base;
   tl.nstrips = (W + sb::WS - 1) / sb::WS;
-  const int pmax = (tl.D - 2 * sb::HB) / 2;
+  if (m != sb::Mode::Fused) tl.ls = tl.L;  // runtime stride: tight packing
   const size_t smem = smem_bytes(tl, m);
+  if (smem > 227 * 1024)
+    return fail(SB_ERR_INVALID_ARGUMENT, "slice radius " + std::to_string(pmax) + " too large for the GPU strip sweep");
   out->smem = smem;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, sb::WS, smem);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  // Residency from the kernel's own resources.  (cudaOccupancyMaxActiveBlocksPerMultiprocessor
+  // reports 1 for kernels that allocate tensor memory, which would idle 3/4 of each SM.)
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+  int smem_per_sm = 233472, regs_per_sm = 65536;
+  cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  const int regs_per_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (sb::WS / 32);
+  occ = std::min(2048 / sb::WS, regs_per_sm / std::max(1, regs_per_cta));
+  occ = std::min<long long>(occ, (long long)smem_per_sm / (long long)(smem + fa.sharedSizeBytes + 1024));
+  if (m == sb::Mode::Fused) occ = std::min(occ, 512 / tl.tmem_cols);
   occ = std::max(occ, 1);
   const long long slots = (long long)sms * occ;
   const long long columns = (long long)tl.nstrips * channels;
@@ -220,6 +216,12 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int W, long 
   tl.rows_per_item = rows_per_item;
   if (columns * items > 0x7fffffffLL) return fail(SB_ERR_INVALID_ARGUMENT, "image too large for the grid");
   out->grid = dim3((unsigned)(tl.nstrips * items), (unsigned)channels, 1);
+  if (std::getenv("SB_DEBUG"))
+    std::fprintf(stderr,
+                 "[sliceblur_b200] mode=%d pmax=%d L=%d ls=%d D=%d tmem_cols=%d packed=%d smem=%zu occ=%d "
+                 "strips=%d items=%lld rows/item=%lld grid=%u x %u\n",
+                 (int)m, pmax, tl.L, tl.ls, tl.D, tl.tmem_cols, tl.packed, smem, occ, tl.nstrips, items, rows_per_item,
+                 out->grid.x, out->grid.y);
   return SB_OK;
 }
 
@@ -304,7 +306,7 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
   if (need == 0) {
     const void* fn = pick_kernel(sb::Mode::Fused, src_dtype, k);
     Launch L;
-    rc = plan_launch(fn, sb::Mode::Fused, base, g.W, total_rows, channels, &L);
+    rc = plan_launch(fn, sb::Mode::Fused, base, plan.pmax, g.W, total_rows, channels, &L);
     if (rc) return rc;
     return launch(fn, L, src, nullptr, nullptr, dst, g, plan.taps, status_dev, st);
   }
@@ -319,13 +321,13 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
   Launch L1;
   sb::Tiling rows_tiling = base;
   rows_tiling.packed = 0;
-  rc = plan_launch(f1, sb::Mode::RowsToMid, rows_tiling, g.W, total_rows, channels, &L1);
+  rc = plan_launch(f1, sb::Mode::RowsToMid, rows_tiling, plan.pmax, g.W, total_rows, channels, &L1);
   if (rc) return rc;
   rc = launch(f1, L1, src, nullptr, mid, nullptr, g, plan.taps, status_dev, st);
   if (rc) return rc;
   const void* f2 = pick_kernel(sb::Mode::ColsFromMid, src_dtype, k);
   Launch L2;
-  rc = plan_launch(f2, sb::Mode::ColsFromMid, base, g.W, total_rows, channels, &L2);
+  rc = plan_launch(f2, sb::Mode::ColsFromMid, base, plan.pmax, g.W, total_rows, channels, &L2);
   if (rc) return rc;
   return launch(f2, L2, nullptr, mid, nullptr, dst, g, plan.taps, status_dev, st);
 }
@@ -356,7 +358,7 @@ int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, 
   g.aligned16 = ((uintptr_t)src % 16 == 0) && ((src_row_stride * g.es) % 16 == 0);
   const void* fn = pick_kernel(sb::Mode::RowsToOut, src_dtype, k);
   Launch L;
-  rc = plan_launch(fn, sb::Mode::RowsToOut, make_tiling(plan.pmax, 1, g.es, false), g.W, rows, 1, &L);
+  rc = plan_launch(fn, sb::Mode::RowsToOut, make_tiling(plan.pmax, 1, g.es, false), plan.pmax, g.W, rows, 1, &L);
   if (rc) return rc;
   return launch(fn, L, src, nullptr, nullptr, dst, g, plan.taps, status_dev, (cudaStream_t)stream);
 }

@@ -1,0 +1,6 @@
+// sweep_f32.cu - instantiations of the sweep kernels for float sources.
+#include "sweep_kernels.cuh"
+
+namespace sb {
+const void* sweep_ptr_f32(Mode m, int k) { return sweep_ptr_for<float>(m, k); }
+}  // namespace sb

@@ -45,6 +45,8 @@ constexpr int HB = 16;          // rows per band
 constexpr int WS = 128;         // strip width = threads per CTA
 constexpr int NWARPS = WS / 32;
 constexpr int CH = 16;          // px per scan chunk (one lane)
+constexpr int LS = 512;         // prefix row stride in words (compile-time: immediate offsets)
+constexpr int LSP = 256;        // packed-prefix row stride in words (uint8, pmax <= 63)
 constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + kMagic rounds x to an integer (|x| < 2^22)
 constexpr int kMagicBits = 0x4B400000;  // bits(kMagic + n) = kMagicBits + n
 constexpr uint32_t kGuard = 0x80008000u;
@@ -74,13 +76,15 @@ struct Taps {
 
 struct Tiling {
   int L;                // staged / prefix row length in px (multiple of 16)
+  int ls;               // prefix row stride in words (LS for the fused mode, >= L)
   int xoff;             // x0 - xb (same for every strip)
   int stage_row_bytes;  // bytes per staged row (multiple of 16)
   int lanes_per_row;    // power of two >= L / CH, <= 32
-  int D;                // ring rows (the ring holds D + HB rows incl. the mirror)
+  int D;                // ring rows, a multiple of HB (the ring holds D + HB rows incl. the mirror)
   int nstrips;          // ceil(W / WS)
   long long rows_per_item;
   int packed;           // uint8 two-rows-per-word prefix
+  int tmem_cols;        // tensor-memory columns allocated for the fused ring (power of two, >= D + HB)
 };
 
 enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3 };
@@ -96,6 +100,37 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 __device__ __forceinline__ void st_stream(float* p, float v) {
   asm volatile("st.global.cs.f32 [%0], %1;\n" ::"l"(p), "f"(v));
+}
+
+// ---- tensor memory (tcgen05): the fused column ring.  Thread c of the CTA owns
+// TMEM lane c (warp w reaches lanes 32w..32w+31); ring slot s is TMEM column s.
+__device__ __forceinline__ void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
 }
 
 template <typename T>
@@ -134,43 +169,37 @@ __device__ __forceinline__ int to_fixed(T v, const Taps& t, bool& bad) {
 // ---------------------------------------------------------------- pass 1: staging
 // Issue the copies of virtual rows v0..v0+n-1 (clamped to the image) of the
 // strip segment [xb, xb+L) into `buf` (row r at buf + r*stage_row_bytes).
+// floor(a / d) for 0 <= a < 2^16 and 1 <= d < 2^15, with magic = 2^32 / d + 1 precomputed
+__device__ __forceinline__ int fast_div(int a, uint32_t magic) { return (int)__umulhi((uint32_t)a, magic); }
+
 template <typename Tin>
 __device__ __forceinline__ void issue_stage(unsigned char* buf, const Tin* __restrict__ src_img, const Geometry& g,
-                                            const Tiling& tl, int xb, int v0, int n) {
-  const int rowbytes_img = g.W * g.in_px * g.es;
-  const int lo = max(xb, 0) * g.in_px * g.es;
-  const int hi = min(xb + tl.L, g.W) * g.in_px * g.es;
+                                            const Tiling& tl, int xb, int v0, int n, int lo, int nchunk,
+                                            uint32_t chunk_magic, int hi16, int hi) {
   const int base = xb * g.in_px * g.es;  // byte of column xb (may be negative)
   if (g.aligned16) {
-    const int lo16 = lo;                 // multiple of 16 (xb is a multiple of 16 px)
-    const int hi16 = hi & ~15;
-    const int nchunk = (hi16 - lo16) >> 4;
     for (int idx = threadIdx.x; idx < n * nchunk; idx += WS) {
-      const int r = idx / nchunk, q = idx - r * nchunk;
+      const int r = fast_div(idx, chunk_magic), q = idx - r * nchunk;
       const int v = min(max(v0 + r, 0), g.H - 1);
       const unsigned char* grow = (const unsigned char*)(src_img + (long long)v * g.in_row);
-      cp_async16(buf + r * tl.stage_row_bytes + (lo16 + 16 * q - base), grow + lo16 + 16 * q);
+      cp_async16(buf + r * tl.stage_row_bytes + (lo + 16 * q - base), grow + lo + 16 * q);
     }
     cp_async_commit();
     if (hi16 < hi) {  // unaligned tail of the last strip (row bytes not a multiple of 16)
       const int tail = hi - hi16;
-      for (int idx = threadIdx.x; idx < n * tail; idx += WS) {
-        const int r = idx / tail, q = idx - r * tail;
+      for (int r = 0; r < n; ++r) {
         const int v = min(max(v0 + r, 0), g.H - 1);
         const unsigned char* grow = (const unsigned char*)(src_img + (long long)v * g.in_row);
-        buf[r * tl.stage_row_bytes + (hi16 + q - base)] = grow[hi16 + q];
+        for (int q = threadIdx.x; q < tail; q += WS) buf[r * tl.stage_row_bytes + (hi16 + q - base)] = grow[hi16 + q];
       }
     }
-    (void)rowbytes_img;
   } else {
     // generic path: element copies (any stride / alignment)
-    const int nel = (hi - lo) / g.es;
-    for (int idx = threadIdx.x; idx < n * nel; idx += WS) {
-      const int r = idx / nel, q = idx - r * nel;
+    const int e0 = lo / g.es, e1 = hi / g.es;
+    for (int r = 0; r < n; ++r) {
       const int v = min(max(v0 + r, 0), g.H - 1);
       const Tin* grow = src_img + (long long)v * g.in_row;
-      const int eoff = lo / g.es + q;
-      *(Tin*)(buf + r * tl.stage_row_bytes + eoff * g.es - base) = grow[eoff];
+      for (int e = e0 + threadIdx.x; e < e1; e += WS) *(Tin*)(buf + r * tl.stage_row_bytes + e * g.es - base) = grow[e];
     }
   }
 }
@@ -178,21 +207,14 @@ __device__ __forceinline__ void issue_stage(unsigned char* buf, const Tin* __res
 // Replicate the border column into staged positions outside [0, W).
 __device__ __forceinline__ void fixup_edges(unsigned char* buf, const Geometry& g, const Tiling& tl, int xb, int n) {
   const int pxb = g.in_px * g.es;
-  const int left = max(0, -xb);                  // positions [0, left) <- column 0
-  const int right0 = max(0, g.W - xb);           // positions [right0, L) <- column W-1
-  const int nright = max(0, tl.L - right0);
-  const int per_row = (left + nright) * pxb;
-  for (int idx = threadIdx.x; idx < n * per_row; idx += WS) {
-    const int r = idx / per_row;
-    int q = idx - r * per_row;
-    const int pos = q / pxb, byte = q - pos * pxb;
+  const int left = max(0, -xb);         // positions [0, left) <- column 0
+  const int right0 = max(0, g.W - xb);  // positions [right0, L) <- column W-1
+  const int lb = left * pxb;
+  const int rb = max(0, tl.L - right0) * pxb;
+  for (int r = 0; r < n; ++r) {
     unsigned char* row = buf + r * tl.stage_row_bytes;
-    if (pos < left) {
-      row[pos * pxb + byte] = row[left * pxb + byte];
-    } else {
-      const int dst = right0 + (pos - left);
-      row[dst * pxb + byte] = row[(right0 - 1) * pxb + byte];
-    }
+    for (int q = threadIdx.x; q < lb; q += WS) row[q] = row[lb + (q % pxb)];
+    for (int q = threadIdx.x; q < rb; q += WS) row[right0 * pxb + q] = row[(right0 - 1) * pxb + (q % pxb)];
   }
 }
 
@@ -246,7 +268,7 @@ __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restr
       }
       const int carry = running + inc - tot;
       if (live) {
-        int4* dst = (int4*)(P + r * tl.L + chunk * CH);
+        int4* dst = (int4*)(P + r * tl.ls + chunk * CH);
 #pragma unroll
         for (int m = 0; m < CH / 4; ++m)
           dst[m] = make_int4(v[4 * m] + carry, v[4 * m + 1] + carry, v[4 * m + 2] + carry, v[4 * m + 3] + carry);
@@ -292,7 +314,7 @@ __device__ __forceinline__ void scan_rows_packed(const unsigned char* buf, uint3
     }
     const uint32_t carry = (inc + kGuard - tot) & kField;  // fieldwise (inc - tot) mod 2^15, no borrow
     if (live) {
-      uint4* dst = (uint4*)(P + q * tl.L + sl * CH);
+      uint4* dst = (uint4*)(P + q * LSP + sl * CH);
 #pragma unroll
       for (int m = 0; m < CH / 4; ++m)
         dst[m] = make_uint4((v[4 * m] + carry) & kField, (v[4 * m + 1] + carry) & kField,
@@ -302,34 +324,71 @@ __device__ __forceinline__ void scan_rows_packed(const unsigned char* buf, uint3
 }
 
 // ---------------------------------------------------------------- pass 1: row values
-// Row-filtered value of staged row r at strip column c (unpacked prefix), in
-// mid quanta (magic-rounded) or, ROW_OUT, in pixel units.
-template <int K, bool ROW_OUT>
-__device__ __forceinline__ float row_value(const int* prow, int c, const Taps& t, const Tiling& tl) {
-  float acc = 0.0f;
+// Row-filtered values of the HB staged rows at strip column c, accumulated box by
+// box so every shared-memory load is (lag pointer) + (row * L): the lag pointers
+// are per-thread constants and the row offsets are uniform.
+template <int K, int STRIDE>
+__device__ __forceinline__ void band_rows(const int* __restrict__ P, int c, const float* __restrict__ w,
+                                          const Taps& t, const Tiling& tl, float (&acc)[HB]) {
+  const int ls = STRIDE ? STRIDE : tl.ls;  // compile-time stride -> immediate load offsets
+#pragma unroll
+  for (int r = 0; r < HB; ++r) acc[r] = 0.0f;
   const int base = c + tl.xoff;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    const int d = prow[base + t.p[i]] - prow[base - t.p[i] - 1];  // exact box sum
-    acc = fmaf(ROW_OUT ? t.w_out1[i] : t.w_row[i], (float)d, acc);
+    const int* pl = P + base + t.p[i];
+    const int* pt = P + base - t.p[i] - 1;
+    const float wi = w[i];
+#pragma unroll
+    for (int r = 0; r < HB; ++r) acc[r] = fmaf(wi, (float)(pl[r * ls] - pt[r * ls]), acc[r]);  // exact box sum
   }
-  return ROW_OUT ? acc : acc + kMagic;
 }
 
-// Rows q and q+8 of a packed band at column c, magic-rounded.
+// Packed uint8 variant: word q holds rows q (bits 0-14) and q+8 (bits 16-30).
 template <int K>
-__device__ __forceinline__ void row_value_packed(const uint32_t* prow, int c, const Taps& t, const Tiling& tl,
-                                                 float& lo_v, float& hi_v) {
-  float a = 0.0f, b = 0.0f;
+__device__ __forceinline__ void band_rows_packed(const uint32_t* __restrict__ P, int c, const Taps& t,
+                                                 const Tiling& tl, float (&acc)[HB]) {
+#pragma unroll
+  for (int r = 0; r < HB; ++r) acc[r] = 0.0f;
   const int base = c + tl.xoff;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    const uint32_t d = prow[base + t.p[i]] + kGuard - prow[base - t.p[i] - 1];
-    a = fmaf(t.w_row[i], (float)(d & 0x7FFFu), a);
-    b = fmaf(t.w_row[i], (float)((d >> 16) & 0x7FFFu), b);
+    const uint32_t* pl = P + base + t.p[i];
+    const uint32_t* pt = P + base - t.p[i] - 1;
+    const float wl = t.w_row[i];
+    const float wh = t.w_row[i] * (1.0f / 65536.0f);  // exact power-of-two scaling
+#pragma unroll
+    for (int q = 0; q < HB / 2; ++q) {
+      const uint32_t d = pl[q * LSP] + kGuard - pt[q * LSP];  // both 15-bit fields, no cross-field borrow
+      acc[q] = fmaf(wl, (float)(d & 0x7FFFu), acc[q]);
+      acc[q + HB / 2] = fmaf(wh, (float)(d & 0x7FFF0000u), acc[q + HB / 2]);
+    }
   }
-  lo_v = a + kMagic;
-  hi_v = b + kMagic;
+}
+
+// Column pass over one output band from the TMEM ring (slot windows contiguous
+// thanks to the mirrored first band): per box two 16-column loads, then the
+// exact running box sum and the weighted output for 16 rows.
+template <int K>
+__device__ __forceinline__ void column_band_tmem(uint32_t tlane, const int (&lead_s)[K], const int (&trail_s)[K],
+                                                 int (&box)[K], const Taps& t, float (&out)[HB]) {
+#pragma unroll
+  for (int r = 0; r < HB; ++r) out[r] = 0.0f;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    uint32_t lv[HB], tv[HB];
+    tmem_ld16(tlane + (uint32_t)lead_s[i], lv);
+    tmem_ld16(tlane + (uint32_t)trail_s[i], tv);
+    tmem_wait_ld();
+    int bx = box[i];
+    const float w = t.w_col[i];
+#pragma unroll
+    for (int r = 0; r < HB; ++r) {
+      bx += (int)lv[r] - (int)tv[r];
+      out[r] = fmaf(w, (float)bx, out[r]);
+    }
+    box[i] = bx;
+  }
 }
 
 // ---------------------------------------------------------------- the sweep kernel
@@ -350,13 +409,27 @@ __global__ void __launch_bounds__(WS) sweep_kernel(const Tin* __restrict__ src, 
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const bool edge = (xb < 0) || (xb + tl.L > g.W);
+  // staged byte range of this strip (same for every row)
+  const int st_lo = max(xb, 0) * g.in_px * g.es;          // multiple of 16 (xb is a multiple of 16 px)
+  const int st_hi = min(xb + tl.L, g.W) * g.in_px * g.es;
+  const int st_hi16 = g.aligned16 ? (st_hi & ~15) : st_hi;
+  const int st_nchunk = max(0, (st_hi16 - st_lo) >> 4);
+  const uint32_t st_magic = 0xFFFFFFFFu / (uint32_t)max(1, st_nchunk) + 1u;
   const bool packed = (sizeof(Tin) == 1) && tl.packed;
 
   // shared-memory carve-up
   unsigned char* stage = smem;                                               // 2 x HB rows
   int* P = (int*)(smem + 2 * HB * tl.stage_row_bytes);                       // HB x L (or HB/2 x L packed)
-  int* ring = (int*)(smem + (M == Mode::ColsFromMid ? 0 : 2 * HB * tl.stage_row_bytes + HB * tl.L * 4));
   const int D = tl.D;
+  uint32_t tlane = 0;  // TMEM address of this warp's lane quarter, column 0
+  if constexpr (M == Mode::Fused) {
+    __shared__ uint32_t tmem_base_s;
+    if (threadIdx.x < 32) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    tlane = tmem_base_s + ((uint32_t)(threadIdx.x & ~31) << 16);
+  }
 
   for (long long T = T0; T < T1;) {
     const int img = (int)(T / g.H);
@@ -398,11 +471,13 @@ __global__ void __launch_bounds__(WS) sweep_kernel(const Tin* __restrict__ src, 
     const int vstart = (M == Mode::Fused) ? a - 1 - t.pmax : a;
     const int count = (M == Mode::Fused) ? (b - a) + 2 * t.pmax + 1 : (b - a);
     const int nbands = (count + HB - 1) / HB;
-    issue_stage<Tin>(stage, src_img, g, tl, xb, vstart, min(HB, count));
+    issue_stage<Tin>(stage, src_img, g, tl, xb, vstart, min(HB, count), st_lo, st_nchunk, st_magic, st_hi16,
+                     st_hi);
 
     int box[K];
-    int lead_s[K], trail_s[K];
-    int out_next = a;  // next output row (Fused)
+    int out_next = a;   // next output row (Fused)
+    int out_mod = 0;    // (out_next - a) mod D
+    int prod_slot = 0;  // ring slot of the next produced row
 #pragma unroll
     for (int i = 0; i < K; ++i) box[i] = 0;
 
@@ -413,7 +488,8 @@ __global__ void __launch_bounds__(WS) sweep_kernel(const Tin* __restrict__ src, 
       __syncthreads();  // staged band visible; everyone done with P and the other buffer
       if (pb + 1 < nbands)
         issue_stage<Tin>(stage + ((pb + 1) & 1) * HB * tl.stage_row_bytes, src_img, g, tl, xb,
-                         vstart + (pb + 1) * HB, min(HB, count - (pb + 1) * HB));
+                         vstart + (pb + 1) * HB, min(HB, count - (pb + 1) * HB), st_lo, st_nchunk, st_magic,
+                         st_hi16, st_hi);
       if (edge) {
         fixup_edges(cur, g, tl, xb, n);
         __syncthreads();
@@ -424,103 +500,124 @@ __global__ void __launch_bounds__(WS) sweep_kernel(const Tin* __restrict__ src, 
         scan_rows<Tin>(cur, P, g, t, tl, ch, n, status);
       __syncthreads();
 
+      float rv[HB];
       if constexpr (M == Mode::RowsToMid || M == Mode::RowsToOut) {
         if (active) {
-          for (int r = 0; r < n; ++r) {
-            const int v = vstart + pb * HB + r;
-            if constexpr (M == Mode::RowsToMid) {
-              float val = row_value<K, false>(P + r * tl.L, c, t, tl);
-              mid_out[ch * g.mid_ch + (long long)img * g.mid_img + (long long)v * g.mid_row + x0 + c] =
-                  __float_as_int(val) - kMagicBits;
-            } else {
-              float val = row_value<K, true>(P + r * tl.L, c, t, tl);
-              dst[(long long)img * g.out_img + (long long)v * g.out_row + (long long)(x0 + c) * g.out_px + ch] = val;
-            }
-          }
-        }
-      } else {  // Fused
-        // row values of this band -> ring (slot = offset mod D, mirrored below HB)
-        const int off0 = pb * HB;
-        if (active) {
-          if (packed) {
-#pragma unroll 2
-            for (int q = 0; q < HB / 2; ++q) {
-              float lo_v, hi_v;
-              row_value_packed<K>((const uint32_t*)P + q * tl.L, c, t, tl, lo_v, hi_v);
-              const int r2[2] = {q, q + HB / 2};
-              const int bits[2] = {__float_as_int(lo_v) - kMagicBits, __float_as_int(hi_v) - kMagicBits};
+          band_rows<K, 0>(P, c, M == Mode::RowsToOut ? t.w_out1 : t.w_row, t, tl, rv);
+          const int v0 = vstart + pb * HB;
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                if (r2[h] < n) {
-                  const int s = (off0 + r2[h]) % D;
-                  ring[s * WS + c] = bits[h];
-                  if (s < HB) ring[(s + D) * WS + c] = bits[h];
-                }
+          for (int r = 0; r < HB; ++r) {
+            if (r < n) {
+              if constexpr (M == Mode::RowsToMid) {
+                mid_out[ch * g.mid_ch + (long long)img * g.mid_img + (long long)(v0 + r) * g.mid_row + x0 + c] =
+                    __float_as_int(rv[r] + kMagic) - kMagicBits;
+              } else {
+                dst[(long long)img * g.out_img + (long long)(v0 + r) * g.out_row + (long long)(x0 + c) * g.out_px +
+                    ch] = rv[r];
               }
             }
-          } else {
-            for (int r = 0; r < n; ++r) {
-              const int bits = __float_as_int(row_value<K, false>(P + r * tl.L, c, t, tl)) - kMagicBits;
-              const int s = (off0 + r) % D;
-              ring[s * WS + c] = bits;
-              if (s < HB) ring[(s + D) * WS + c] = bits;
-            }
           }
         }
-        const int produced = off0 + n;
-        // box sums at row a-1 once rows a-1-pmax .. a-1+pmax (offsets 0..2pmax) exist
-        if (active && produced >= 2 * t.pmax + 1 && produced - n < 2 * t.pmax + 1) {
-          for (int u = 0; u <= 2 * t.pmax; ++u) {
-            const int val = ring[(u % D) * WS + c];
-            const int au = u > t.pmax ? u - t.pmax : t.pmax - u;
+      } else {  // Fused: all threads take part (tcgen05 ops are warp-collective)
+        if (packed)
+          band_rows_packed<K>((const uint32_t*)P, c, t, tl, rv);
+        else
+          band_rows<K, LS>(P, c, t.w_row, t, tl, rv);
+        {
+          // band pb -> TMEM columns [prod_slot, prod_slot + HB) (D is a multiple of HB);
+          // the first band is mirrored at column D so lag windows never wrap
+          uint32_t bits[HB];
 #pragma unroll
-            for (int i = 0; i < K; ++i)
-              if (au <= t.p[i]) box[i] += val;
+          for (int r = 0; r < HB; ++r) bits[r] = (uint32_t)(__float_as_int(rv[r] + kMagic) - kMagicBits);
+          tmem_st16(tlane + (uint32_t)prod_slot, bits);
+          if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, bits);
+          tmem_wait_st();
+        }
+        const int produced = pb * HB + n;
+        prod_slot += HB;
+        prod_slot = prod_slot >= D ? 0 : prod_slot;
+        // box sums at row a-1 once rows a-1-pmax .. a-1+pmax (columns 0..2pmax) exist
+        if (produced >= 2 * t.pmax + 1 && produced - n < 2 * t.pmax + 1) {
+          for (int u0 = 0; u0 <= 2 * t.pmax; u0 += HB) {
+            uint32_t v[HB];
+            tmem_ld16(tlane + (uint32_t)u0, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < HB; ++j) {
+              const int u = u0 + j;
+              const int au = u > t.pmax ? u - t.pmax : t.pmax - u;
+#pragma unroll
+              for (int i = 0; i < K; ++i)
+                if (u <= 2 * t.pmax && au <= t.p[i]) box[i] += (int)v[j];
+            }
           }
         }
         // emit every output band whose lead rows are in the ring
         while (out_next < b) {
           const int nb = min(HB, b - out_next);
-          const int need = (out_next - a) + nb + 2 * t.pmax + 1;  // offsets required
-          if (produced < need && produced < count) break;
+          const int need = (out_next - a) + nb + 2 * t.pmax + 1;  // ring rows required
+          if (produced < need) break;
+          int lead_s[K], trail_s[K];
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            const int l = out_mod + t.pmax + 1 + t.p[i];  // row out_next + p_i
+            const int tr = out_mod + t.pmax - t.p[i];     // row out_next - p_i - 1
+            lead_s[i] = l >= D ? l - D : l;
+            trail_s[i] = tr >= D ? tr - D : tr;
+          }
+          float ov[HB];
+          column_band_tmem<K>(tlane, lead_s, trail_s, box, t, ov);
           if (active) {
-            const int ob = out_next - a;  // offset of output row out_next relative to a
-#pragma unroll
-            for (int i = 0; i < K; ++i) {
-              lead_s[i] = (ob + t.pmax + 1 + t.p[i]) % D;   // row out_next + p_i
-              trail_s[i] = (ob + t.pmax - t.p[i]) % D;      // row out_next - p_i - 1
-            }
-            float* dcol = dst + (long long)img * g.out_img + (long long)out_next * g.out_row +
+            float* dptr = dst + (long long)img * g.out_img + (long long)out_next * g.out_row +
                           (long long)(x0 + c) * g.out_px + ch;
-            if (nb == HB) {
 #pragma unroll
-              for (int r = 0; r < HB; ++r) {
-                float acc = 0.0f;
-#pragma unroll
-                for (int i = 0; i < K; ++i) {
-                  box[i] += ring[(lead_s[i] + r) * WS + c] - ring[(trail_s[i] + r) * WS + c];
-                  acc = fmaf(t.w_col[i], (float)box[i], acc);
-                }
-                st_stream(dcol + (long long)r * g.out_row, acc);
-              }
-            } else {
-              for (int r = 0; r < nb; ++r) {
-                float acc = 0.0f;
-#pragma unroll
-                for (int i = 0; i < K; ++i) {
-                  box[i] += ring[(lead_s[i] + r) * WS + c] - ring[(trail_s[i] + r) * WS + c];
-                  acc = fmaf(t.w_col[i], (float)box[i], acc);
-                }
-                st_stream(dcol + (long long)r * g.out_row, acc);
-              }
-            }
+            for (int r = 0; r < HB; ++r)
+              if (r < nb) st_stream(dptr + (long long)r * g.out_row, ov[r]);
           }
           out_next += nb;
+          out_mod += nb;
+          out_mod = out_mod >= D ? out_mod - D : out_mod;
         }
       }
     }
     __syncthreads();  // P / stage reuse by the next segment
   }
+  if constexpr (M == Mode::Fused) {
+    tmem_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tmem_dealloc(tlane, (uint32_t)tl.tmem_cols);
+  }
+}
+
+// Kernel pointers per source type, instantiated in sweep_<dtype>.cu (one
+// translation unit each, compiled in parallel).
+const void* sweep_ptr_u8(Mode m, int k);
+const void* sweep_ptr_u16(Mode m, int k);
+const void* sweep_ptr_f32(Mode m, int k);
+const void* sweep_ptr_f64(Mode m, int k);
+const void* sweep_ptr_cols(int k);  // ColsFromMid (source type unused)
+
+template <typename Tin>
+const void* sweep_ptr_for(Mode m, int k) {
+#define SB_K_CASES(MODE)                                         \
+  switch (k) {                                                   \
+    case 1: return (const void*)sweep_kernel<Tin, 1, MODE>;      \
+    case 2: return (const void*)sweep_kernel<Tin, 2, MODE>;      \
+    case 3: return (const void*)sweep_kernel<Tin, 3, MODE>;      \
+    case 4: return (const void*)sweep_kernel<Tin, 4, MODE>;      \
+    case 5: return (const void*)sweep_kernel<Tin, 5, MODE>;      \
+    case 6: return (const void*)sweep_kernel<Tin, 6, MODE>;      \
+    case 7: return (const void*)sweep_kernel<Tin, 7, MODE>;      \
+    default: return (const void*)sweep_kernel<Tin, 8, MODE>;     \
+  }
+  switch (m) {
+    case Mode::Fused: SB_K_CASES(Mode::Fused)
+    case Mode::RowsToMid: SB_K_CASES(Mode::RowsToMid)
+    case Mode::RowsToOut: SB_K_CASES(Mode::RowsToOut)
+    default: break;
+  }
+  return nullptr;
+#undef SB_K_CASES
 }
 
 }  // namespace sb
