@@ -136,7 +136,7 @@ sb::Tiling make_tiling(int pmax, int channels, int es, bool u8_single) {
   tl.stage_row_bytes = ceil16(tl.L * channels * es);
   tl.ls = tl.L <= sb::LS ? sb::LS : tl.L;  // the fused kernel is compiled for stride LS
   tl.D = ((2 * pmax + 2 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;  // multiple of HB
-  tl.packed = (u8_single && (2 * pmax + 1) * 255 < 32768 && nchunk <= 32 && tl.L <= sb::LSP) ? 1 : 0;
+  tl.packed = (u8_single && nchunk <= 32 && tl.L <= sb::LSP) ? 1 : 0;  // exact 16-bit prefixes
   int cols = 32;
   while (cols < tl.D + sb::HB) cols <<= 1;
   tl.tmem_cols = cols;
@@ -145,16 +145,18 @@ sb::Tiling make_tiling(int pmax, int channels, int es, bool u8_single) {
 
 size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
   if (m == sb::Mode::ColsFromMid) return 0;
-  const size_t prefix = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP * sizeof(int) : (size_t)sb::HB * tl.ls * sizeof(int);
-  size_t s = (size_t)2 * sb::HB * tl.stage_row_bytes + prefix;
+  const size_t stage = (size_t)2 * sb::HB * tl.stage_row_bytes;
   if (m == sb::Mode::Fused) {
-    // the ring lives in tensor memory: cap residency at 512 / tmem_cols CTAs per SM by
-    // asking for enough shared memory, so no CTA ever waits inside tcgen05.alloc
+    // two prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
+    const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP * sizeof(int) : (size_t)sb::HB * sb::LS * sizeof(int);
+    size_t s = (size_t)sb::NSTAGE * sb::HB * tl.stage_row_bytes + 2 * pbuf;
+    // cap residency at 512 / tmem_cols CTAs per SM by asking for enough shared
+    // memory, so no CTA ever waits inside tcgen05.alloc
     const int ctas = 512 / tl.tmem_cols;
     const size_t floor_bytes = 233472 / (size_t)(ctas + 1) - 1024 + 16;
-    s = std::max(s, floor_bytes);
+    return std::max(s, floor_bytes);
   }
-  return s;
+  return stage + (size_t)sb::HB * tl.ls * sizeof(int);
 }
 
 bool fused_fits(int pmax, int channels, int es) {
@@ -199,8 +201,9 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, in
   int smem_per_sm = 233472, regs_per_sm = 65536;
   cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   cudaDeviceGetAttribute(&regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-  const int regs_per_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (sb::WS / 32);
-  occ = std::min(2048 / sb::WS, regs_per_sm / std::max(1, regs_per_cta));
+  const int threads = (m == sb::Mode::Fused) ? sb::FUSED_THREADS : sb::WS;
+  const int regs_per_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (threads / 32);
+  occ = std::min(2048 / threads, regs_per_sm / std::max(1, regs_per_cta));
   occ = std::min<long long>(occ, (long long)smem_per_sm / (long long)(smem + fa.sharedSizeBytes + 1024));
   if (m == sb::Mode::Fused) occ = std::min(occ, 512 / tl.tmem_cols);
   occ = std::max(occ, 1);
@@ -230,6 +233,14 @@ int launch(const void* fn, const Launch& L, const void* src, const int* mid_in, 
   void* args[] = {(void*)&src, (void*)&mid_in, (void*)&mid_out, (void*)&dst,
                   (void*)&g,   (void*)&t,      (void*)&L.tl,    (void*)&status};
   cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::WS), args, L.smem, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+  return SB_OK;
+}
+
+int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, const sb::Geometry& g,
+                 const sb::Taps& t, int* status, cudaStream_t stream) {
+  void* args[] = {(void*)&src, (void*)&dst, (void*)&g, (void*)&t, (void*)&L.tl, (void*)&status};
+  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::FUSED_THREADS), args, L.smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   return SB_OK;
 }
@@ -308,7 +319,7 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
     Launch L;
     rc = plan_launch(fn, sb::Mode::Fused, base, plan.pmax, g.W, total_rows, channels, &L);
     if (rc) return rc;
-    return launch(fn, L, src, nullptr, nullptr, dst, g, plan.taps, status_dev, st);
+    return launch_fused(fn, L, src, dst, g, plan.taps, status_dev, st);
   }
   // two launches through an int32 workspace laid out [channel][batch][H][W]
   if (!workspace || workspace_bytes < need)

@@ -49,8 +49,6 @@ constexpr int LS = 512;         // prefix row stride in words (compile-time: imm
 constexpr int LSP = 256;        // packed-prefix row stride in words (uint8, pmax <= 63)
 constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + kMagic rounds x to an integer (|x| < 2^22)
 constexpr int kMagicBits = 0x4B400000;  // bits(kMagic + n) = kMagicBits + n
-constexpr uint32_t kGuard = 0x80008000u;
-constexpr uint32_t kField = 0x7FFF7FFFu;
 
 struct Geometry {
   long long in_img, in_row;    // source strides (elements)
@@ -98,6 +96,8 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 __device__ __forceinline__ void st_stream(float* p, float v) {
   asm volatile("st.global.cs.f32 [%0], %1;\n" ::"l"(p), "f"(v));
 }
@@ -131,6 +131,33 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr)
       : "memory");
+}
+
+// ---- mbarriers (producer/consumer hand-off inside a CTA)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t@!p "
+      "bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// int32 -> fp32 through the full-rate I2FP.F32.S32 path: the inline cvt hides the
+// operand's range, so the compiler cannot pick the slow I2F.U16 form for 16-bit values.
+__device__ __forceinline__ float i2f_fast(uint32_t x) {
+  float f;
+  asm("cvt.rn.f32.s32 %0, %1;" : "=f"(f) : "r"(x));
+  return f;
 }
 
 template <typename T>
@@ -175,10 +202,11 @@ __device__ __forceinline__ int fast_div(int a, uint32_t magic) { return (int)__u
 template <typename Tin>
 __device__ __forceinline__ void issue_stage(unsigned char* buf, const Tin* __restrict__ src_img, const Geometry& g,
                                             const Tiling& tl, int xb, int v0, int n, int lo, int nchunk,
-                                            uint32_t chunk_magic, int hi16, int hi) {
+                                            uint32_t chunk_magic, int hi16, int hi, int tid = threadIdx.x,
+                                            int nthr = WS) {
   const int base = xb * g.in_px * g.es;  // byte of column xb (may be negative)
   if (g.aligned16) {
-    for (int idx = threadIdx.x; idx < n * nchunk; idx += WS) {
+    for (int idx = tid; idx < n * nchunk; idx += nthr) {
       const int r = fast_div(idx, chunk_magic), q = idx - r * nchunk;
       const int v = min(max(v0 + r, 0), g.H - 1);
       const unsigned char* grow = (const unsigned char*)(src_img + (long long)v * g.in_row);
@@ -190,7 +218,7 @@ __device__ __forceinline__ void issue_stage(unsigned char* buf, const Tin* __res
       for (int r = 0; r < n; ++r) {
         const int v = min(max(v0 + r, 0), g.H - 1);
         const unsigned char* grow = (const unsigned char*)(src_img + (long long)v * g.in_row);
-        for (int q = threadIdx.x; q < tail; q += WS) buf[r * tl.stage_row_bytes + (hi16 + q - base)] = grow[hi16 + q];
+        for (int q = tid; q < tail; q += nthr) buf[r * tl.stage_row_bytes + (hi16 + q - base)] = grow[hi16 + q];
       }
     }
   } else {
@@ -199,22 +227,31 @@ __device__ __forceinline__ void issue_stage(unsigned char* buf, const Tin* __res
     for (int r = 0; r < n; ++r) {
       const int v = min(max(v0 + r, 0), g.H - 1);
       const Tin* grow = src_img + (long long)v * g.in_row;
-      for (int e = e0 + threadIdx.x; e < e1; e += WS) *(Tin*)(buf + r * tl.stage_row_bytes + e * g.es - base) = grow[e];
+      for (int e = e0 + tid; e < e1; e += nthr) *(Tin*)(buf + r * tl.stage_row_bytes + e * g.es - base) = grow[e];
     }
   }
 }
 
 // Replicate the border column into staged positions outside [0, W).
-__device__ __forceinline__ void fixup_edges(unsigned char* buf, const Geometry& g, const Tiling& tl, int xb, int n) {
+__device__ __forceinline__ void fixup_edges(unsigned char* buf, const Geometry& g, const Tiling& tl, int xb, int n,
+                                            int tid = threadIdx.x, int nthr = WS) {
   const int pxb = g.in_px * g.es;
   const int left = max(0, -xb);         // positions [0, left) <- column 0
   const int right0 = max(0, g.W - xb);  // positions [right0, L) <- column W-1
   const int lb = left * pxb;
   const int rb = max(0, tl.L - right0) * pxb;
+  if (pxb == 1) {
+    for (int r = 0; r < n; ++r) {
+      unsigned char* row = buf + r * tl.stage_row_bytes;
+      for (int q = tid; q < lb; q += nthr) row[q] = row[lb];
+      for (int q = tid; q < rb; q += nthr) row[right0 + q] = row[right0 - 1];
+    }
+    return;
+  }
   for (int r = 0; r < n; ++r) {
     unsigned char* row = buf + r * tl.stage_row_bytes;
-    for (int q = threadIdx.x; q < lb; q += WS) row[q] = row[lb + (q % pxb)];
-    for (int q = threadIdx.x; q < rb; q += WS) row[right0 * pxb + q] = row[(right0 - 1) * pxb + (q % pxb)];
+    for (int q = tid; q < lb; q += nthr) row[q] = row[lb + (q % pxb)];
+    for (int q = tid; q < rb; q += nthr) row[right0 * pxb + q] = row[(right0 - 1) * pxb + (q % pxb)];
   }
 }
 
@@ -222,14 +259,15 @@ __device__ __forceinline__ void fixup_edges(unsigned char* buf, const Geometry& 
 // Inclusive modular int32 prefix of `n` staged rows, channel `ch`, into P[r][j].
 template <typename Tin>
 __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restrict__ P, const Geometry& g,
-                                          const Taps& t, const Tiling& tl, int ch, int n, int* status) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                          const Taps& t, const Tiling& tl, int ch, int n, int* status,
+                                          int warp = threadIdx.x >> 5, int nwarps = NWARPS) {
+  const int lane = threadIdx.x & 31;
   const int lpr = tl.lanes_per_row;
   const int rows_per_warp = 32 / lpr;
   const int sub = lane / lpr, sl = lane - sub * lpr;
   const int nchunk = tl.L / CH;
   bool bad = false;
-  for (int r0 = warp * rows_per_warp; r0 < n; r0 += NWARPS * rows_per_warp) {
+  for (int r0 = warp * rows_per_warp; r0 < n; r0 += nwarps * rows_per_warp) {
     const int r = r0 + sub;
     int running = 0;  // prefix of the chunk groups already done (rows longer than lpr chunks)
     for (int cg = 0; cg < nchunk; cg += lpr) {
@@ -279,15 +317,18 @@ __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restr
   if (bad && status) atomicOr(status, SB_STATUS_RANGE);
 }
 
-// uint8, one channel: rows q and q+8 of the band share P word q (15-bit fields).
+// uint8, one channel: rows q and q+8 of the band share P word q as two exact
+// 16-bit prefixes (L <= 256 staged bytes, so a prefix is at most 256*255 < 2^16
+// and is monotone: lead - trail never borrows across the fields).
 __device__ __forceinline__ void scan_rows_packed(const unsigned char* buf, uint32_t* __restrict__ P,
-                                                 const Tiling& tl) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                                 const Tiling& tl, int warp = threadIdx.x >> 5,
+                                                 int nwarps = NWARPS) {
+  const int lane = threadIdx.x & 31;
   const int lpr = tl.lanes_per_row;
   const int pairs_per_warp = 32 / lpr;
   const int sub = lane / lpr, sl = lane - sub * lpr;
   const int nchunk = tl.L / CH;
-  for (int q0 = warp * pairs_per_warp; q0 < HB / 2; q0 += NWARPS * pairs_per_warp) {
+  for (int q0 = warp * pairs_per_warp; q0 < HB / 2; q0 += nwarps * pairs_per_warp) {
     const int q = q0 + sub;
     const bool live = (q < HB / 2) && (sl < nchunk);
     uint32_t v[CH];
@@ -299,9 +340,10 @@ __device__ __forceinline__ void scan_rows_packed(const unsigned char* buf, uint3
       const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
       for (int m = 0; m < CH; ++m) {
+        // {a_m, 0, b_m, 0}: byte m of row q in field 0, of row q+8 in field 1
         const uint32_t lo = __byte_perm(aw[m >> 2], 0u, 0x4440u | (m & 3));
         const uint32_t hi = __byte_perm(bw[m >> 2], 0u, 0x4044u | ((m & 3) << 8));
-        tot = tot + lo + hi;  // < 16*255 per field: no carry between fields
+        tot = tot + lo + hi;
         v[m] = tot;
       }
     }
@@ -310,15 +352,14 @@ __device__ __forceinline__ void scan_rows_packed(const unsigned char* buf, uint3
     for (int o = 1; o < 32; o <<= 1) {
       if (o >= lpr) break;
       uint32_t y = __shfl_up_sync(0xffffffffu, inc, o, lpr);
-      if (sl >= o) inc = (inc + y) & kField;
+      if (sl >= o) inc += y;
     }
-    const uint32_t carry = (inc + kGuard - tot) & kField;  // fieldwise (inc - tot) mod 2^15, no borrow
+    const uint32_t carry = inc - tot;
     if (live) {
       uint4* dst = (uint4*)(P + q * LSP + sl * CH);
 #pragma unroll
       for (int m = 0; m < CH / 4; ++m)
-        dst[m] = make_uint4((v[4 * m] + carry) & kField, (v[4 * m + 1] + carry) & kField,
-                            (v[4 * m + 2] + carry) & kField, (v[4 * m + 3] + carry) & kField);
+        dst[m] = make_uint4(v[4 * m] + carry, v[4 * m + 1] + carry, v[4 * m + 2] + carry, v[4 * m + 3] + carry);
     }
   }
 }
@@ -344,7 +385,7 @@ __device__ __forceinline__ void band_rows(const int* __restrict__ P, int c, cons
   }
 }
 
-// Packed uint8 variant: word q holds rows q (bits 0-14) and q+8 (bits 16-30).
+// Packed uint8 variant: word q holds rows q (bits 0-15) and q+8 (bits 16-31).
 template <int K>
 __device__ __forceinline__ void band_rows_packed(const uint32_t* __restrict__ P, int c, const Taps& t,
                                                  const Tiling& tl, float (&acc)[HB]) {
@@ -356,12 +397,11 @@ __device__ __forceinline__ void band_rows_packed(const uint32_t* __restrict__ P,
     const uint32_t* pl = P + base + t.p[i];
     const uint32_t* pt = P + base - t.p[i] - 1;
     const float wl = t.w_row[i];
-    const float wh = t.w_row[i] * (1.0f / 65536.0f);  // exact power-of-two scaling
 #pragma unroll
     for (int q = 0; q < HB / 2; ++q) {
-      const uint32_t d = pl[q * LSP] + kGuard - pt[q * LSP];  // both 15-bit fields, no cross-field borrow
-      acc[q] = fmaf(wl, (float)(d & 0x7FFFu), acc[q]);
-      acc[q + HB / 2] = fmaf(wh, (float)(d & 0x7FFF0000u), acc[q + HB / 2]);
+      const uint32_t d = pl[q * LSP] - pt[q * LSP];  // two exact 16-bit box sums
+      acc[q] = fmaf(wl, i2f_fast(d & 0xFFFFu), acc[q]);
+      acc[q + HB / 2] = fmaf(wl, i2f_fast(d >> 16), acc[q + HB / 2]);
     }
   }
 }
@@ -528,7 +568,7 @@ __global__ void __launch_bounds__(WS) sweep_kernel(const Tin* __restrict__ src, 
           // the first band is mirrored at column D so lag windows never wrap
           uint32_t bits[HB];
 #pragma unroll
-          for (int r = 0; r < HB; ++r) bits[r] = (uint32_t)(__float_as_int(rv[r] + kMagic) - kMagicBits);
+          for (int r = 0; r < HB; ++r) bits[r] = (uint32_t)__float_as_int(rv[r] + kMagic);  // kMagicBits-biased
           tmem_st16(tlane + (uint32_t)prod_slot, bits);
           if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, bits);
           tmem_wait_st();
@@ -548,7 +588,7 @@ __global__ void __launch_bounds__(WS) sweep_kernel(const Tin* __restrict__ src, 
               const int au = u > t.pmax ? u - t.pmax : t.pmax - u;
 #pragma unroll
               for (int i = 0; i < K; ++i)
-                if (u <= 2 * t.pmax && au <= t.p[i]) box[i] += (int)v[j];
+                if (u <= 2 * t.pmax && au <= t.p[i]) box[i] += (int)v[j] - kMagicBits;
             }
           }
         }
@@ -570,9 +610,20 @@ __global__ void __launch_bounds__(WS) sweep_kernel(const Tin* __restrict__ src, 
           if (active) {
             float* dptr = dst + (long long)img * g.out_img + (long long)out_next * g.out_row +
                           (long long)(x0 + c) * g.out_px + ch;
+            const long long step = g.out_row;
+            if (nb == HB) {
 #pragma unroll
-            for (int r = 0; r < HB; ++r)
-              if (r < nb) st_stream(dptr + (long long)r * g.out_row, ov[r]);
+              for (int r = 0; r < HB; ++r) {
+                st_stream(dptr, ov[r]);
+                dptr += step;
+              }
+            } else {
+#pragma unroll
+              for (int r = 0; r < HB; ++r) {
+                if (r < nb) st_stream(dptr, ov[r]);
+                dptr += step;
+              }
+            }
           }
           out_next += nb;
           out_mod += nb;
@@ -587,6 +638,199 @@ __global__ void __launch_bounds__(WS) sweep_kernel(const Tin* __restrict__ src, 
     __syncthreads();
     if (threadIdx.x < 32) tmem_dealloc(tlane, (uint32_t)tl.tmem_cols);
   }
+}
+
+// ---------------------------------------------------------------- fused, warp-specialised
+// CTA = NCONS consumer warps (thread c <-> strip column c <-> TMEM lane c) and
+// NPROD producer warps.  Producers stage rows with cp.async (one band ahead),
+// replicate edge columns and prefix-scan each band into one of two prefix
+// buffers; consumers turn a prefix buffer into row values (releasing it
+// immediately), append them to the TMEM ring and emit every output band whose
+// rows are all present.  Buffers are handed over with mbarriers, so consumers
+// never wait on a CTA-wide barrier.
+constexpr int NCONS = WS / 32;
+constexpr int NPROD = 2;
+constexpr int FUSED_THREADS = 32 * (NCONS + NPROD);
+constexpr int NSTAGE = 2 * NPROD;  // staged bands (each producer warp double-buffers its own)
+
+template <typename Tin, int K>
+__global__ void __launch_bounds__(FUSED_THREADS, 3)
+    fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2];
+  const int strip = blockIdx.x % tl.nstrips;
+  const long long item = blockIdx.x / tl.nstrips;
+  const int ch = blockIdx.y;
+  const int x0 = strip * WS;
+  const int xb = x0 - tl.xoff;
+  const int warp = threadIdx.x >> 5;
+  const bool producer = warp >= NCONS;
+  const long long total = (long long)g.nimg * g.H;
+  const long long T0 = item * tl.rows_per_item;
+  const long long T1 = min(T0 + tl.rows_per_item, total);
+  const bool packed = (sizeof(Tin) == 1) && tl.packed;
+  const int pbuf_words = packed ? (HB / 2) * LSP : HB * LS;
+  unsigned char* stage = smem;                                       // 2 producers x 2 staged bands
+  int* Pbase = (int*)(smem + NSTAGE * HB * tl.stage_row_bytes);      // 2 prefix buffers
+  const int D = tl.D;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_full[0], 32);  // one producer warp fills a prefix buffer
+    mbar_init(&bar_full[1], 32);
+    mbar_init(&bar_empty[0], 32 * NCONS);
+    mbar_init(&bar_empty[1], 32 * NCONS);
+  }
+  if (warp == 0) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+
+  if (producer) {
+    // ------------------------------------------------ producer warps
+    // Producer warp pw owns the bands with global index gb = pw (mod 2): it stages
+    // them into its private pair of buffers (prefetching its next band) and scans
+    // them into prefix buffer pw, so the producers never synchronise with each other.
+    const int lane = threadIdx.x & 31, pw = warp - NCONS;
+    const bool edge = (xb < 0) || (xb + tl.L > g.W);
+    const int st_lo = max(xb, 0) * g.in_px * g.es;
+    const int st_hi = min(xb + tl.L, g.W) * g.in_px * g.es;
+    const int st_hi16 = g.aligned16 ? (st_hi & ~15) : st_hi;
+    const int st_nchunk = max(0, (st_hi16 - st_lo) >> 4);
+    const uint32_t st_magic = 0xFFFFFFFFu / (uint32_t)max(1, st_nchunk) + 1u;
+    unsigned char* mystage = stage + pw * 2 * HB * tl.stage_row_bytes;
+    int* P = Pbase + pw * pbuf_words;
+    uint32_t gb0 = 0;  // global index of the segment's first band
+    for (long long T = T0; T < T1;) {
+      const int img = (int)(T / g.H);
+      const int a = (int)(T - (long long)img * g.H);
+      const int b = (int)min((long long)g.H, T1 - (long long)img * g.H);
+      T = (long long)img * g.H + b;
+      const Tin* src_img = src + (long long)img * g.in_img;
+      const int vstart = a - 1 - t.pmax;
+      const int count = (b - a) + 2 * t.pmax + 1;
+      const int nbands = (count + HB - 1) / HB;
+      const int first = (int)((pw - gb0) & 1u);  // first band of this segment owned by this warp
+      if (first < nbands)
+        issue_stage<Tin>(mystage, src_img, g, tl, xb, vstart + first * HB, min(HB, count - first * HB), st_lo,
+                         st_nchunk, st_magic, st_hi16, st_hi, lane, 32);
+      int sb = 0;
+      for (int pb = first; pb < nbands; pb += 2, sb ^= 1) {
+        const uint32_t gb = gb0 + pb;
+        const int n = min(HB, count - pb * HB);
+        unsigned char* cur = mystage + sb * HB * tl.stage_row_bytes;
+        cp_async_wait_all();  // this band landed (the next one is issued below)
+        __syncwarp();
+        if (pb + 2 < nbands)
+          issue_stage<Tin>(mystage + (sb ^ 1) * HB * tl.stage_row_bytes, src_img, g, tl, xb, vstart + (pb + 2) * HB,
+                           min(HB, count - (pb + 2) * HB), st_lo, st_nchunk, st_magic, st_hi16, st_hi, lane, 32);
+        if (edge) {
+          fixup_edges(cur, g, tl, xb, n, lane, 32);
+          __syncwarp();
+        }
+        mbar_wait(&bar_empty[pw], ((gb >> 1) & 1) ^ 1);  // consumers done with prefix buffer pw
+        if (packed)
+          scan_rows_packed(cur, (uint32_t*)P, tl, 0, 1);
+        else
+          scan_rows<Tin>(cur, P, g, t, tl, ch, n, status, 0, 1);
+        mbar_arrive(&bar_full[pw]);
+      }
+      gb0 += (uint32_t)nbands;
+    }
+  } else {
+    // ------------------------------------------------ consumer warps
+    const int c = threadIdx.x;
+    const bool active = (x0 + c) < g.W;
+    const uint32_t tlane = tmem_base_s + ((uint32_t)(threadIdx.x & ~31) << 16);
+    uint32_t gb = 0;
+    for (long long T = T0; T < T1;) {
+      const int img = (int)(T / g.H);
+      const int a = (int)(T - (long long)img * g.H);
+      const int b = (int)min((long long)g.H, T1 - (long long)img * g.H);
+      T = (long long)img * g.H + b;
+      const int count = (b - a) + 2 * t.pmax + 1;
+      const int nbands = (count + HB - 1) / HB;
+      int box[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) box[i] = 0;
+      int out_next = a, out_mod = 0, prod_slot = 0;
+      for (int pb = 0; pb < nbands; ++pb, ++gb) {
+        const int n = min(HB, count - pb * HB);
+        const int* P = Pbase + (gb & 1) * pbuf_words;
+        float rv[HB];
+        mbar_wait(&bar_full[gb & 1], (gb >> 1) & 1);
+        if (packed)
+          band_rows_packed<K>((const uint32_t*)P, c, t, tl, rv);
+        else
+          band_rows<K, LS>(P, c, t.w_row, t, tl, rv);
+        mbar_arrive(&bar_empty[gb & 1]);
+        {
+          uint32_t bits[HB];
+#pragma unroll
+          for (int r = 0; r < HB; ++r) bits[r] = (uint32_t)__float_as_int(rv[r] + kMagic);  // kMagicBits-biased
+          tmem_st16(tlane + (uint32_t)prod_slot, bits);
+          if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, bits);  // mirror: lag windows never wrap
+          tmem_wait_st();
+        }
+        const int produced = pb * HB + n;
+        prod_slot += HB;
+        prod_slot = prod_slot >= D ? 0 : prod_slot;
+        if (produced >= 2 * t.pmax + 1 && produced - n < 2 * t.pmax + 1) {
+          for (int u0 = 0; u0 <= 2 * t.pmax; u0 += HB) {
+            uint32_t v[HB];
+            tmem_ld16(tlane + (uint32_t)u0, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < HB; ++j) {
+              const int u = u0 + j;
+              const int au = u > t.pmax ? u - t.pmax : t.pmax - u;
+#pragma unroll
+              for (int i = 0; i < K; ++i)
+                if (u <= 2 * t.pmax && au <= t.p[i]) box[i] += (int)v[j] - kMagicBits;
+            }
+          }
+        }
+        while (out_next < b) {
+          const int nb = min(HB, b - out_next);
+          if (produced < (out_next - a) + nb + 2 * t.pmax + 1) break;
+          int lead_s[K], trail_s[K];
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            const int l = out_mod + t.pmax + 1 + t.p[i];
+            const int tr = out_mod + t.pmax - t.p[i];
+            lead_s[i] = l >= D ? l - D : l;
+            trail_s[i] = tr >= D ? tr - D : tr;
+          }
+          float ov[HB];
+          column_band_tmem<K>(tlane, lead_s, trail_s, box, t, ov);
+          if (active) {
+            float* dptr = dst + (long long)img * g.out_img + (long long)out_next * g.out_row +
+                          (long long)(x0 + c) * g.out_px + ch;
+            const long long step = g.out_row;
+            if (nb == HB) {
+#pragma unroll
+              for (int r = 0; r < HB; ++r) {
+                st_stream(dptr, ov[r]);
+                dptr += step;
+              }
+            } else {
+#pragma unroll
+              for (int r = 0; r < HB; ++r) {
+                if (r < nb) st_stream(dptr, ov[r]);
+                dptr += step;
+              }
+            }
+          }
+          out_next += nb;
+          out_mod += nb;
+          out_mod = out_mod >= D ? out_mod - D : out_mod;
+        }
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem_base_s, (uint32_t)tl.tmem_cols);
 }
 
 // Kernel pointers per source type, instantiated in sweep_<dtype>.cu (one
@@ -610,8 +854,19 @@ const void* sweep_ptr_for(Mode m, int k) {
     case 7: return (const void*)sweep_kernel<Tin, 7, MODE>;      \
     default: return (const void*)sweep_kernel<Tin, 8, MODE>;     \
   }
+  if (m == Mode::Fused) {
+    switch (k) {
+      case 1: return (const void*)fused_kernel<Tin, 1>;
+      case 2: return (const void*)fused_kernel<Tin, 2>;
+      case 3: return (const void*)fused_kernel<Tin, 3>;
+      case 4: return (const void*)fused_kernel<Tin, 4>;
+      case 5: return (const void*)fused_kernel<Tin, 5>;
+      case 6: return (const void*)fused_kernel<Tin, 6>;
+      case 7: return (const void*)fused_kernel<Tin, 7>;
+      default: return (const void*)fused_kernel<Tin, 8>;
+    }
+  }
   switch (m) {
-    case Mode::Fused: SB_K_CASES(Mode::Fused)
     case Mode::RowsToMid: SB_K_CASES(Mode::RowsToMid)
     case Mode::RowsToOut: SB_K_CASES(Mode::RowsToOut)
     default: break;
