@@ -247,7 +247,8 @@ def run_ours(args, cfg):
     import ctypes
 
     rp = np.ascontiguousarray(kern.radii, np.int64)
-    ws = lib.sb_separable_filter_2d_workspace_bytes(cfg["batch"], cfg["h"], cfg["w"], cfg["channels"],
+    dcode = nat.SB_DTYPE_U8 if cfg["dtype"] == "u8" else nat.SB_DTYPE_F32
+    ws = lib.sb_separable_filter_2d_workspace_bytes(dcode, cfg["batch"], cfg["h"], cfg["w"], cfg["channels"],
                                                     rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), kern.k)
     launches_per_step = 1 if ws == 0 else 2 * cfg["channels"]
 

@@ -73,11 +73,11 @@ const char* sb_last_error(void);
  * SB_ERR_NOT_UNIT_DC if |sum w_i (2 p_i + 1) - 1| > 1e-6, else SB_OK. */
 int sb_check_kernel(const int64_t* radii, const double* weights, int k, int64_t extent);
 
-/* Bytes of device workspace sb_separable_filter_2d needs for this shape
- * (0 when the single fused kernel applies; the size of the int32
- * intermediate when the radius needs the two-kernel path). */
-size_t sb_separable_filter_2d_workspace_bytes(int64_t batch, int64_t height, int64_t width, int channels,
-                                              const int64_t* radii, int k);
+/* Bytes of device workspace sb_separable_filter_2d needs for this source
+ * type and shape (0 when the single fused kernel applies; the size of the
+ * int32 intermediate when the radius needs the two-kernel path). */
+size_t sb_separable_filter_2d_workspace_bytes(int src_dtype, int64_t batch, int64_t height, int64_t width,
+                                              int channels, const int64_t* radii, int k);
 
 /* filtering.py:76-104 separable_filter_2d over a batch of images:
  *   dst[b, y, x, c] = cols(rows(src[b, :, :, c]))[y, x]

@@ -64,7 +64,7 @@ def _declare(lib):
     lib.sb_last_error.restype = ctypes.c_char_p
     lib.sb_check_kernel.argtypes = [_i64p, _f64p, _int, _i64]
     lib.sb_check_kernel.restype = _int
-    lib.sb_separable_filter_2d_workspace_bytes.argtypes = [_i64, _i64, _i64, _int, _i64p, _int]
+    lib.sb_separable_filter_2d_workspace_bytes.argtypes = [_int, _i64, _i64, _i64, _int, _i64p, _int]
     lib.sb_separable_filter_2d_workspace_bytes.restype = _size
     lib.sb_separable_filter_2d.argtypes = [
         _vp, _int, _i64, _i64, _i64, _int, _i64, _i64,  # src, dtype, batch, h, w, channels, img/row stride

@@ -123,20 +123,33 @@ struct Launch {
 };
 
 // Tiling of a strip sweep (see sweep_kernels.cuh): staged/prefix row [xb, xb+L)
-// with xb = x0 - xoff, ring of D + HB rows for the fused mode.
-sb::Tiling make_tiling(int pmax, int channels, int es, bool u8_single) {
+// with xb = x0 - xoff for a strip of `sw` columns; ring of D rows (+ HB mirror).
+sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_single) {
   sb::Tiling tl;
   std::memset(&tl, 0, sizeof(tl));
   tl.xoff = ceil16(pmax + 1);
-  tl.L = ceil16(tl.xoff + sb::WS + pmax);
+  tl.sw = sb::WS;
+  const bool rows_only = (m == sb::Mode::RowsToMid || m == sb::Mode::RowsToOut);
+  const int staged_ch = rows_only ? 1 : channels;  // the row pass gathers its channel
+  if (rows_only) {
+    // widen the strip until the halo costs <= 50% extra (bounded by shared memory)
+    while (tl.sw < 1024 && ceil16(tl.xoff + tl.sw + pmax) > (3 * tl.sw) / 2) {
+      const int L2 = ceil16(tl.xoff + 2 * tl.sw + pmax);
+      if ((size_t)2 * sb::HB * ceil16(L2 * es) + (size_t)sb::HB * L2 * 4 > kSmemBudget) break;
+      tl.sw *= 2;
+    }
+  }
+  tl.L = ceil16(tl.xoff + tl.sw + pmax);
   const int nchunk = tl.L / sb::CH;
   int lpr = 1;
   while (lpr < nchunk && lpr < 32) lpr <<= 1;
   tl.lanes_per_row = lpr;
-  tl.stage_row_bytes = ceil16(tl.L * channels * es);
-  tl.ls = tl.L <= sb::LS ? sb::LS : tl.L;  // the fused kernel is compiled for stride LS
+  tl.stage_row_bytes = ceil16(tl.L * staged_ch * es);
+  tl.ls = (m == sb::Mode::Fused) ? sb::LS : tl.L;
+  tl.packed = (m == sb::Mode::Fused && u8_single && nchunk <= 32 && tl.L <= sb::LSP) ? 1 : 0;  // exact 16-bit prefixes
+  tl.npb = tl.packed ? 2 : 1;  // unpacked prefix buffers are large: one per producer
   tl.D = ((2 * pmax + 2 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;  // multiple of HB
-  tl.packed = (u8_single && nchunk <= 32 && tl.L <= sb::LSP) ? 1 : 0;  // exact 16-bit prefixes
+  if (m == sb::Mode::ColsFromMid) tl.D = std::min(tl.D, 512 - sb::HB);  // deeper trails come from the plane
   int cols = 32;
   while (cols < tl.D + sb::HB) cols <<= 1;
   tl.tmem_cols = cols;
@@ -145,22 +158,21 @@ sb::Tiling make_tiling(int pmax, int channels, int es, bool u8_single) {
 
 size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
   if (m == sb::Mode::ColsFromMid) return 0;
-  const size_t stage = (size_t)2 * sb::HB * tl.stage_row_bytes;
   if (m == sb::Mode::Fused) {
-    // two prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
+    // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
     const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP * sizeof(int) : (size_t)sb::HB * sb::LS * sizeof(int);
-    size_t s = (size_t)sb::NSTAGE * sb::HB * tl.stage_row_bytes + 2 * pbuf;
+    size_t s = (size_t)sb::NSTAGE * sb::HB * tl.stage_row_bytes + (size_t)sb::NPROD * tl.npb * pbuf;
     // cap residency at 512 / tmem_cols CTAs per SM by asking for enough shared
     // memory, so no CTA ever waits inside tcgen05.alloc
     const int ctas = 512 / tl.tmem_cols;
     const size_t floor_bytes = 233472 / (size_t)(ctas + 1) - 1024 + 16;
     return std::max(s, floor_bytes);
   }
-  return stage + (size_t)sb::HB * tl.ls * sizeof(int);
+  return (size_t)2 * sb::HB * tl.stage_row_bytes + (size_t)sb::HB * tl.ls * sizeof(int);
 }
 
 bool fused_fits(int pmax, int channels, int es) {
-  sb::Tiling tl = make_tiling(pmax, channels, es, false);
+  sb::Tiling tl = make_tiling(sb::Mode::Fused, pmax, channels, es, false);
   return tl.L <= sb::LS && tl.tmem_cols <= 512 && smem_bytes(tl, sb::Mode::Fused) <= kSmemBudget;
 }
 
@@ -182,8 +194,7 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, in
                 int channels, Launch* out) {
   sb::Tiling& tl = out->tl;
   tl = base;
-  tl.nstrips = (W + sb::WS - 1) / sb::WS;
-  if (m != sb::Mode::Fused) tl.ls = tl.L;  // runtime stride: tight packing
+  tl.nstrips = (W + tl.sw - 1) / tl.sw;
   const size_t smem = smem_bytes(tl, m);
   if (smem > 227 * 1024)
     return fail(SB_ERR_INVALID_ARGUMENT, "slice radius " + std::to_string(pmax) + " too large for the GPU strip sweep");
@@ -205,14 +216,28 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, in
   const int regs_per_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (threads / 32);
   occ = std::min(2048 / threads, regs_per_sm / std::max(1, regs_per_cta));
   occ = std::min<long long>(occ, (long long)smem_per_sm / (long long)(smem + fa.sharedSizeBytes + 1024));
-  if (m == sb::Mode::Fused) occ = std::min(occ, 512 / tl.tmem_cols);
+  if (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid) occ = std::min(occ, 512 / tl.tmem_cols);
   occ = std::max(occ, 1);
   const long long slots = (long long)sms * occ;
   const long long columns = (long long)tl.nstrips * channels;
-  long long items = std::max(1LL, slots / columns);
   const bool sweeps = (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid);
-  const long long min_rows = sweeps ? 8LL * (2 * pmax + 1) : sb::HB;
-  items = std::min(items, std::max(1LL, total_rows / min_rows));
+  // Column sweeps pay 2*pmax+1 warm-up rows per item; the row pass pays nothing.
+  // Pick the item count minimising (waves of CTAs) x (rows per item incl. warm-up).
+  const long long warm = sweeps ? 2LL * pmax + 1 : 0;
+  const long long max_items = std::max(1LL, std::min<long long>(4096, total_rows / std::max<long long>(sb::HB, warm)));
+  long long best_items = 1;
+  double best_cost = 1e300;
+  for (long long it = 1; it <= max_items; ++it) {
+    const long long ctas = columns * it;
+    const long long waves = (ctas + slots - 1) / slots;
+    const long long rows = (total_rows + it - 1) / it;
+    const double cost = (double)waves * (double)(rows + warm + sb::HB);
+    if (cost < best_cost * 0.995) {
+      best_cost = cost;
+      best_items = it;
+    }
+  }
+  long long items = best_items;
   long long rows_per_item = (total_rows + items - 1) / items;
   if (!sweeps) rows_per_item = ((rows_per_item + sb::HB - 1) / sb::HB) * sb::HB;
   items = (total_rows + rows_per_item - 1) / rows_per_item;
@@ -228,10 +253,17 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, in
   return SB_OK;
 }
 
-int launch(const void* fn, const Launch& L, const void* src, const int* mid_in, int* mid_out, float* dst,
-           const sb::Geometry& g, const sb::Taps& t, int* status, cudaStream_t stream) {
-  void* args[] = {(void*)&src, (void*)&mid_in, (void*)&mid_out, (void*)&dst,
-                  (void*)&g,   (void*)&t,      (void*)&L.tl,    (void*)&status};
+int launch_rows(const void* fn, const Launch& L, const void* src, int* mid_out, float* dst, const sb::Geometry& g,
+                const sb::Taps& t, int* status, cudaStream_t stream) {
+  void* args[] = {(void*)&src, (void*)&mid_out, (void*)&dst, (void*)&g, (void*)&t, (void*)&L.tl, (void*)&status};
+  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::WS), args, L.smem, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+  return SB_OK;
+}
+
+int launch_cols(const void* fn, const Launch& L, const int* mid_in, float* dst, const sb::Geometry& g,
+                const sb::Taps& t, cudaStream_t stream) {
+  void* args[] = {(void*)&mid_in, (void*)&dst, (void*)&g, (void*)&t, (void*)&L.tl};
   cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::WS), args, L.smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   return SB_OK;
@@ -249,7 +281,7 @@ int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, c
 
 extern "C" {
 
-int sb_version(void) { return 1; }
+int sb_version(void) { return 2; }
 
 const char* sb_last_error(void) { return g_last_error.c_str(); }
 
@@ -265,11 +297,12 @@ int sb_check_kernel(const int64_t* radii, const double* weights, int k, int64_t 
   return SB_OK;
 }
 
-size_t sb_separable_filter_2d_workspace_bytes(int64_t batch, int64_t height, int64_t width, int channels,
-                                              const int64_t* radii, int k) {
+size_t sb_separable_filter_2d_workspace_bytes(int src_dtype, int64_t batch, int64_t height, int64_t width,
+                                              int channels, const int64_t* radii, int k) {
   if (!radii || k < 1 || k > SB_MAX_K || batch < 1 || height < 1 || width < 1 || channels < 1) return 0;
-  // the dtype only changes the staged bytes; decide with the widest common one (f32)
-  if (fused_fits((int)radii[k - 1], channels, 4)) return 0;
+  const int es = dtype_size(src_dtype);
+  if (es == 0) return 0;
+  if (fused_fits((int)radii[k - 1], channels, es)) return 0;
   return (size_t)batch * height * width * channels * sizeof(int);
 }
 
@@ -311,9 +344,9 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
                 (batch == 1 || (src_image_stride * g.es) % 16 == 0);
   const long long total_rows = (long long)batch * height;
   const bool u8_single = (src_dtype == SB_DTYPE_U8 && channels == 1);
-  const sb::Tiling base = make_tiling(plan.pmax, channels, g.es, u8_single);
+  const sb::Tiling base = make_tiling(sb::Mode::Fused, plan.pmax, channels, g.es, u8_single);
 
-  const size_t need = sb_separable_filter_2d_workspace_bytes(batch, height, width, channels, radii, k);
+  const size_t need = sb_separable_filter_2d_workspace_bytes(src_dtype, batch, height, width, channels, radii, k);
   if (need == 0) {
     const void* fn = pick_kernel(sb::Mode::Fused, src_dtype, k);
     Launch L;
@@ -328,19 +361,41 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
   g.mid_row = width;
   g.mid_img = (long long)height * width;
   g.mid_ch = g.mid_img * batch;
+  // streaming row pass (full-width bands, prefix carried across chunks) when it applies
+  const int xs = -(((plan.pmax + 1) + 15) & ~15);  // first halo column, 16-aligned
+  const int lagc = (sb::CW - 1 - xs + plan.pmax) / sb::CW;
+  if (src_dtype == SB_DTYPE_F32 && lagc + 1 < sb::NSLOT) {
+    const void* fs = sb::sweep_ptr_stream_f32(k);
+    const size_t smem = (size_t)sb::NPROD * 2 * 8 * sb::CW * sizeof(float) + (size_t)sb::HB * sb::RL * sizeof(int);
+    cudaError_t e = cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int nb_total = (int)((total_rows + sb::HB - 1) / sb::HB);
+    const int gx = std::max(1, std::min(nb_total, sms * 2 * 8 / std::max(1, channels)));
+    void* args[] = {(void*)&src, (void*)&mid, (void*)&g, (void*)&plan.taps, (void*)&xs, (void*)&nb_total,
+                    (void*)&status_dev};
+    if (std::getenv("SB_DEBUG"))
+      std::fprintf(stderr, "[sliceblur_b200] stream rows: pmax=%d xs=%d lagc=%d bands=%d grid=%d x %d smem=%zu\n",
+                   plan.pmax, xs, lagc, nb_total, gx, channels, smem);
+    e = cudaLaunchKernel(fs, dim3(gx, channels), dim3(sb::FUSED_THREADS), args, smem, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+  } else {
   const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);
   Launch L1;
-  sb::Tiling rows_tiling = base;
-  rows_tiling.packed = 0;
-  rc = plan_launch(f1, sb::Mode::RowsToMid, rows_tiling, plan.pmax, g.W, total_rows, channels, &L1);
+  rc = plan_launch(f1, sb::Mode::RowsToMid, make_tiling(sb::Mode::RowsToMid, plan.pmax, channels, g.es, false),
+                   plan.pmax, g.W, total_rows, channels, &L1);
   if (rc) return rc;
-  rc = launch(f1, L1, src, nullptr, mid, nullptr, g, plan.taps, status_dev, st);
+  rc = launch_rows(f1, L1, src, mid, nullptr, g, plan.taps, status_dev, st);
   if (rc) return rc;
+  }
   const void* f2 = pick_kernel(sb::Mode::ColsFromMid, src_dtype, k);
   Launch L2;
-  rc = plan_launch(f2, sb::Mode::ColsFromMid, base, plan.pmax, g.W, total_rows, channels, &L2);
+  rc = plan_launch(f2, sb::Mode::ColsFromMid, make_tiling(sb::Mode::ColsFromMid, plan.pmax, channels, 4, false),
+                   plan.pmax, g.W, total_rows, channels, &L2);
   if (rc) return rc;
-  return launch(f2, L2, nullptr, mid, nullptr, dst, g, plan.taps, status_dev, st);
+  return launch_cols(f2, L2, mid, dst, g, plan.taps, st);
 }
 
 int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, int64_t src_row_stride, float* dst,
@@ -369,9 +424,10 @@ int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, 
   g.aligned16 = ((uintptr_t)src % 16 == 0) && ((src_row_stride * g.es) % 16 == 0);
   const void* fn = pick_kernel(sb::Mode::RowsToOut, src_dtype, k);
   Launch L;
-  rc = plan_launch(fn, sb::Mode::RowsToOut, make_tiling(plan.pmax, 1, g.es, false), plan.pmax, g.W, rows, 1, &L);
+  rc = plan_launch(fn, sb::Mode::RowsToOut, make_tiling(sb::Mode::RowsToOut, plan.pmax, 1, g.es, false), plan.pmax,
+                   g.W, rows, 1, &L);
   if (rc) return rc;
-  return launch(fn, L, src, nullptr, nullptr, dst, g, plan.taps, status_dev, (cudaStream_t)stream);
+  return launch_rows(fn, L, src, nullptr, dst, g, plan.taps, status_dev, (cudaStream_t)stream);
 }
 
 int sb_slice_filter_1d(const void* src, int src_dtype, int64_t n, float* dst, const int64_t* radii,

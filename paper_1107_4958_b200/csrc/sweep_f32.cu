@@ -3,4 +3,5 @@
 
 namespace sb {
 const void* sweep_ptr_f32(Mode m, int k) { return sweep_ptr_for<float>(m, k); }
+const void* sweep_ptr_stream_f32(int k) { return stream_ptr_for_f32(k); }
 }  // namespace sb

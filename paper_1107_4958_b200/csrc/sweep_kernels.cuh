@@ -82,7 +82,9 @@ struct Tiling {
   int nstrips;          // ceil(W / WS)
   long long rows_per_item;
   int packed;           // uint8 two-rows-per-word prefix
-  int tmem_cols;        // tensor-memory columns allocated for the fused ring (power of two, >= D + HB)
+  int tmem_cols;        // tensor-memory columns allocated for the ring (power of two, >= D + HB)
+  int sw;               // strip width in columns (WS for sweeps, wider for the row pass alone)
+  int npb;              // fused: prefix buffers per producer warp (1 or 2)
 };
 
 enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3 };
@@ -143,7 +145,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t@!p "
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p "
       "bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -328,6 +330,7 @@ __device__ __forceinline__ void scan_rows_packed(const unsigned char* buf, uint3
   const int pairs_per_warp = 32 / lpr;
   const int sub = lane / lpr, sl = lane - sub * lpr;
   const int nchunk = tl.L / CH;
+#pragma unroll 4
   for (int q0 = warp * pairs_per_warp; q0 < HB / 2; q0 += nwarps * pairs_per_warp) {
     const int q = q0 + sub;
     const bool live = (q < HB / 2) && (sl < nchunk);
@@ -431,213 +434,240 @@ __device__ __forceinline__ void column_band_tmem(uint32_t tlane, const int (&lea
   }
 }
 
-// ---------------------------------------------------------------- the sweep kernel
-// Grid: x = nstrips * items, y = channel.  Block: WS threads.
+// ---------------------------------------------------------------- row pass alone
+// RowsToMid (two-launch path for large radii: int32 R plane, magic-rounded to
+// the mid quantum) and RowsToOut (slice_filter_1d / _filter_rows: float rows).
+// A CTA owns a strip of tl.sw columns (a multiple of WS; wide strips keep the
+// 2*pmax+1 halo small) and walks down a contiguous range of rows in bands of
+// HB, staging with cp.async one band ahead.  Multi-channel (interleaved)
+// sources gather only this CTA's channel (4-byte cp.async), so shared memory
+// holds one channel.
 template <typename Tin, int K, Mode M>
-__global__ void __launch_bounds__(WS) sweep_kernel(const Tin* __restrict__ src, const int* __restrict__ mid_in,
-                                                   int* __restrict__ mid_out, float* __restrict__ dst, Geometry g,
-                                                   Taps t, Tiling tl, int* status) {
+__global__ void __launch_bounds__(WS) rows_kernel(const Tin* __restrict__ src, int* __restrict__ mid_out,
+                                                  float* __restrict__ dst, Geometry g, Taps t, Tiling tl,
+                                                  int* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int strip = blockIdx.x % tl.nstrips;
   const long long item = blockIdx.x / tl.nstrips;
   const int ch = blockIdx.y;
-  const int x0 = strip * WS;
+  const int x0 = strip * tl.sw;
   const int xb = x0 - tl.xoff;
-  const int c = threadIdx.x;
-  const bool active = (x0 + c) < g.W;
   const long long total = (long long)g.nimg * g.H;
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const bool edge = (xb < 0) || (xb + tl.L > g.W);
-  // staged byte range of this strip (same for every row)
-  const int st_lo = max(xb, 0) * g.in_px * g.es;          // multiple of 16 (xb is a multiple of 16 px)
+  // staged source layout: gather = one channel, contiguous; otherwise the raw interleaved bytes
+  const bool gather = g.in_px > 1;
+  Geometry gs = g;  // geometry of the staged buffer as the scan sees it
+  if (gather) {
+    gs.in_px = 1;
+    gs.W = g.W;
+  }
+  const int st_lo = max(xb, 0) * g.in_px * g.es;
   const int st_hi = min(xb + tl.L, g.W) * g.in_px * g.es;
   const int st_hi16 = g.aligned16 ? (st_hi & ~15) : st_hi;
   const int st_nchunk = max(0, (st_hi16 - st_lo) >> 4);
   const uint32_t st_magic = 0xFFFFFFFFu / (uint32_t)max(1, st_nchunk) + 1u;
-  const bool packed = (sizeof(Tin) == 1) && tl.packed;
+  unsigned char* stage = smem;
+  int* P = (int*)(smem + 2 * HB * tl.stage_row_bytes);
 
-  // shared-memory carve-up
-  unsigned char* stage = smem;                                               // 2 x HB rows
-  int* P = (int*)(smem + 2 * HB * tl.stage_row_bytes);                       // HB x L (or HB/2 x L packed)
-  const int D = tl.D;
-  uint32_t tlane = 0;  // TMEM address of this warp's lane quarter, column 0
-  if constexpr (M == Mode::Fused) {
-    __shared__ uint32_t tmem_base_s;
-    if (threadIdx.x < 32) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    tlane = tmem_base_s + ((uint32_t)(threadIdx.x & ~31) << 16);
-  }
+  auto stage_band = [&](unsigned char* buf, const Tin* src_img, int v0, int n) {
+    if (!gather) {
+      issue_stage<Tin>(buf, src_img, g, tl, xb, v0, n, st_lo, st_nchunk, st_magic, st_hi16, st_hi);
+      return;
+    }
+    const int e0 = max(xb, 0), e1 = min(xb + tl.L, g.W);
+    const int cnt = e1 - e0;
+    for (int r = 0; r < n; ++r) {
+      const int v = min(max(v0 + r, 0), g.H - 1);
+      const Tin* grow = src_img + (long long)v * g.in_row + ch;
+      Tin* srow = (Tin*)(buf + r * tl.stage_row_bytes) + (e0 - xb);
+      for (int e = threadIdx.x; e < cnt; e += WS) {
+        if constexpr (sizeof(Tin) == 4) {
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(srow + e)),
+                       "l"(grow + (long long)(e0 + e) * g.in_px));
+        } else {
+          srow[e] = grow[(long long)(e0 + e) * g.in_px];
+        }
+      }
+    }
+    cp_async_commit();
+  };
 
   for (long long T = T0; T < T1;) {
     const int img = (int)(T / g.H);
     const int a = (int)(T - (long long)img * g.H);
     const int b = (int)min((long long)g.H, T1 - (long long)img * g.H);
     T = (long long)img * g.H + b;
-    const Tin* src_img = src ? src + (long long)img * g.in_img : nullptr;
-
-    if constexpr (M == Mode::ColsFromMid) {
-      // Column sweep straight from the int32 R plane (large radii).
-      if (!active) continue;
-      const int* mcol = mid_in + ch * g.mid_ch + (long long)img * g.mid_img + x0 + c;
-      auto R = [&](int v) { return mcol[(long long)min(max(v, 0), g.H - 1) * g.mid_row]; };
-      int box[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) box[i] = 0;
-      for (int u = -t.pmax; u <= t.pmax; ++u) {
-        const int val = R(a - 1 + u);
-        const int au = u < 0 ? -u : u;
-#pragma unroll
-        for (int i = 0; i < K; ++i)
-          if (au <= t.p[i]) box[i] += val;
-      }
-      float* dcol = dst + (long long)img * g.out_img + (long long)(x0 + c) * g.out_px + ch;
-      for (int y = a; y < b; ++y) {
-        float acc = 0.0f;
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-          box[i] += R(y + t.p[i]) - R(y - t.p[i] - 1);
-          acc = fmaf(t.w_col[i], (float)box[i], acc);
-        }
-        st_stream(dcol + (long long)y * g.out_row, acc);
-      }
-      continue;
-    }
-
-    // ---- pass-1 producer shared by all other modes
-    // virtual rows to produce: [vstart, vstart + count)
-    const int vstart = (M == Mode::Fused) ? a - 1 - t.pmax : a;
-    const int count = (M == Mode::Fused) ? (b - a) + 2 * t.pmax + 1 : (b - a);
+    const Tin* src_img = src + (long long)img * g.in_img;
+    const int count = b - a;
     const int nbands = (count + HB - 1) / HB;
-    issue_stage<Tin>(stage, src_img, g, tl, xb, vstart, min(HB, count), st_lo, st_nchunk, st_magic, st_hi16,
-                     st_hi);
-
-    int box[K];
-    int out_next = a;   // next output row (Fused)
-    int out_mod = 0;    // (out_next - a) mod D
-    int prod_slot = 0;  // ring slot of the next produced row
-#pragma unroll
-    for (int i = 0; i < K; ++i) box[i] = 0;
-
+    stage_band(stage, src_img, a, min(HB, count));
     for (int pb = 0; pb < nbands; ++pb) {
       const int n = min(HB, count - pb * HB);
       unsigned char* cur = stage + (pb & 1) * HB * tl.stage_row_bytes;
       cp_async_wait_all();
       __syncthreads();  // staged band visible; everyone done with P and the other buffer
-      if (pb + 1 < nbands)
-        issue_stage<Tin>(stage + ((pb + 1) & 1) * HB * tl.stage_row_bytes, src_img, g, tl, xb,
-                         vstart + (pb + 1) * HB, min(HB, count - (pb + 1) * HB), st_lo, st_nchunk, st_magic,
-                         st_hi16, st_hi);
+      if (pb + 1 < nbands) stage_band(stage + ((pb + 1) & 1) * HB * tl.stage_row_bytes, src_img, a + (pb + 1) * HB,
+                                      min(HB, count - (pb + 1) * HB));
       if (edge) {
-        fixup_edges(cur, g, tl, xb, n);
+        fixup_edges(cur, gs, tl, xb, n);
         __syncthreads();
       }
-      if (packed)
-        scan_rows_packed(cur, (uint32_t*)P, tl);
-      else
-        scan_rows<Tin>(cur, P, g, t, tl, ch, n, status);
+      scan_rows<Tin>(cur, P, gs, t, tl, gather ? 0 : ch, n, status);
       __syncthreads();
-
-      float rv[HB];
-      if constexpr (M == Mode::RowsToMid || M == Mode::RowsToOut) {
-        if (active) {
-          band_rows<K, 0>(P, c, M == Mode::RowsToOut ? t.w_out1 : t.w_row, t, tl, rv);
-          const int v0 = vstart + pb * HB;
+      const int v0 = a + pb * HB;
+      for (int c = threadIdx.x; c < tl.sw; c += WS) {
+        if (x0 + c >= g.W) break;
+        float rv[HB];
+        band_rows<K, 0>(P, c, M == Mode::RowsToOut ? t.w_out1 : t.w_row, t, tl, rv);
 #pragma unroll
-          for (int r = 0; r < HB; ++r) {
-            if (r < n) {
-              if constexpr (M == Mode::RowsToMid) {
-                mid_out[ch * g.mid_ch + (long long)img * g.mid_img + (long long)(v0 + r) * g.mid_row + x0 + c] =
-                    __float_as_int(rv[r] + kMagic) - kMagicBits;
-              } else {
-                dst[(long long)img * g.out_img + (long long)(v0 + r) * g.out_row + (long long)(x0 + c) * g.out_px +
-                    ch] = rv[r];
-              }
-            }
-          }
-        }
-      } else {  // Fused: all threads take part (tcgen05 ops are warp-collective)
-        if (packed)
-          band_rows_packed<K>((const uint32_t*)P, c, t, tl, rv);
-        else
-          band_rows<K, LS>(P, c, t.w_row, t, tl, rv);
-        {
-          // band pb -> TMEM columns [prod_slot, prod_slot + HB) (D is a multiple of HB);
-          // the first band is mirrored at column D so lag windows never wrap
-          uint32_t bits[HB];
-#pragma unroll
-          for (int r = 0; r < HB; ++r) bits[r] = (uint32_t)__float_as_int(rv[r] + kMagic);  // kMagicBits-biased
-          tmem_st16(tlane + (uint32_t)prod_slot, bits);
-          if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, bits);
-          tmem_wait_st();
-        }
-        const int produced = pb * HB + n;
-        prod_slot += HB;
-        prod_slot = prod_slot >= D ? 0 : prod_slot;
-        // box sums at row a-1 once rows a-1-pmax .. a-1+pmax (columns 0..2pmax) exist
-        if (produced >= 2 * t.pmax + 1 && produced - n < 2 * t.pmax + 1) {
-          for (int u0 = 0; u0 <= 2 * t.pmax; u0 += HB) {
-            uint32_t v[HB];
-            tmem_ld16(tlane + (uint32_t)u0, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < HB; ++j) {
-              const int u = u0 + j;
-              const int au = u > t.pmax ? u - t.pmax : t.pmax - u;
-#pragma unroll
-              for (int i = 0; i < K; ++i)
-                if (u <= 2 * t.pmax && au <= t.p[i]) box[i] += (int)v[j] - kMagicBits;
-            }
-          }
-        }
-        // emit every output band whose lead rows are in the ring
-        while (out_next < b) {
-          const int nb = min(HB, b - out_next);
-          const int need = (out_next - a) + nb + 2 * t.pmax + 1;  // ring rows required
-          if (produced < need) break;
-          int lead_s[K], trail_s[K];
-#pragma unroll
-          for (int i = 0; i < K; ++i) {
-            const int l = out_mod + t.pmax + 1 + t.p[i];  // row out_next + p_i
-            const int tr = out_mod + t.pmax - t.p[i];     // row out_next - p_i - 1
-            lead_s[i] = l >= D ? l - D : l;
-            trail_s[i] = tr >= D ? tr - D : tr;
-          }
-          float ov[HB];
-          column_band_tmem<K>(tlane, lead_s, trail_s, box, t, ov);
-          if (active) {
-            float* dptr = dst + (long long)img * g.out_img + (long long)out_next * g.out_row +
-                          (long long)(x0 + c) * g.out_px + ch;
-            const long long step = g.out_row;
-            if (nb == HB) {
-#pragma unroll
-              for (int r = 0; r < HB; ++r) {
-                st_stream(dptr, ov[r]);
-                dptr += step;
-              }
+        for (int r = 0; r < HB; ++r) {
+          if (r < n) {
+            if constexpr (M == Mode::RowsToMid) {
+              mid_out[ch * g.mid_ch + (long long)img * g.mid_img + (long long)(v0 + r) * g.mid_row + x0 + c] =
+                  __float_as_int(rv[r] + kMagic) - kMagicBits;
             } else {
-#pragma unroll
-              for (int r = 0; r < HB; ++r) {
-                if (r < nb) st_stream(dptr, ov[r]);
-                dptr += step;
-              }
+              dst[(long long)img * g.out_img + (long long)(v0 + r) * g.out_row + (long long)(x0 + c) * g.out_px + ch] =
+                  rv[r];
             }
           }
-          out_next += nb;
-          out_mod += nb;
-          out_mod = out_mod >= D ? out_mod - D : out_mod;
         }
       }
     }
     __syncthreads();  // P / stage reuse by the next segment
   }
-  if constexpr (M == Mode::Fused) {
-    tmem_fence_before();
-    __syncthreads();
-    if (threadIdx.x < 32) tmem_dealloc(tlane, (uint32_t)tl.tmem_cols);
+}
+
+// ---------------------------------------------------------------- column pass from the int32 plane
+// ColsFromMid (large radii): thread c <-> strip column c <-> TMEM lane c.  Each
+// band of HB rows of the R plane is read once (coalesced, one band ahead into
+// registers) and appended to a TMEM ring of D rows (mirrored first band); the
+// k running box sums read their lead/trail windows from the ring, except
+// trails older than the ring (lag > D - HB) which are re-read from the plane
+// (L2-resident: the plane rows a CTA touched 2*pmax rows ago).
+template <int K>
+__global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in, float* __restrict__ dst, Geometry g,
+                                                  Taps t, Tiling tl) {
+  __shared__ uint32_t tmem_base_s;
+  const int strip = blockIdx.x % tl.nstrips;
+  const long long item = blockIdx.x / tl.nstrips;
+  const int ch = blockIdx.y;
+  const int x0 = strip * WS;
+  const int c = threadIdx.x;
+  const bool active = (x0 + c) < g.W;
+  const int xc = active ? x0 + c : g.W - 1;  // inactive lanes mirror a valid column (no stores)
+  const long long total = (long long)g.nimg * g.H;
+  const long long T0 = item * tl.rows_per_item;
+  const long long T1 = min(T0 + tl.rows_per_item, total);
+  const int D = tl.D;
+  if (threadIdx.x < 32) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tlane = tmem_base_s + ((uint32_t)(threadIdx.x & ~31) << 16);
+
+  for (long long T = T0; T < T1;) {
+    const int img = (int)(T / g.H);
+    const int a = (int)(T - (long long)img * g.H);
+    const int b = (int)min((long long)g.H, T1 - (long long)img * g.H);
+    T = (long long)img * g.H + b;
+    const int* mcol = mid_in + ch * g.mid_ch + (long long)img * g.mid_img + xc;
+    const long long mrow = g.mid_row;
+    // rows of one band, clamped only where the band crosses the image top or bottom
+    auto load_band = [&](int v0, uint32_t (&dst_)[HB]) {
+      if (v0 >= 0 && v0 + HB <= g.H) {
+        const int* p = mcol + (long long)v0 * mrow;
+#pragma unroll
+        for (int r = 0; r < HB; ++r) dst_[r] = (uint32_t)__ldg(p + r * mrow);
+      } else {
+#pragma unroll
+        for (int r = 0; r < HB; ++r) dst_[r] = (uint32_t)__ldg(mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
+      }
+    };
+    const int vstart = a - 1 - t.pmax;
+    const int count = (b - a) + 2 * t.pmax + 1;
+    const int nbands = (count + HB - 1) / HB;
+    int box[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) box[i] = 0;
+    // ring slots of the lead / in-ring trail windows of the next output band, advanced by HB
+    // per band with one conditional wrap (D is a multiple of HB)
+    int lead_s[K], trail_s[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      lead_s[i] = (t.pmax + 1 + t.p[i]) % D;
+      trail_s[i] = (t.pmax - t.p[i]) % D;
+    }
+    int out_next = a, prod_slot = 0;
+    uint32_t nxt[HB];
+    load_band(vstart, nxt);
+    for (int pb = 0; pb < nbands; ++pb) {
+      const int n = min(HB, count - pb * HB);
+      uint32_t cur[HB];
+#pragma unroll
+      for (int r = 0; r < HB; ++r) cur[r] = nxt[r];
+      if (pb + 1 < nbands) load_band(vstart + (pb + 1) * HB, nxt);
+      tmem_st16(tlane + (uint32_t)prod_slot, cur);
+      if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, cur);
+      tmem_wait_st();
+      const int produced = pb * HB + n;
+      prod_slot += HB;
+      prod_slot = prod_slot >= D ? 0 : prod_slot;
+      if (produced >= 2 * t.pmax + 1 && produced - n < 2 * t.pmax + 1) {
+        for (int u = 0; u <= 2 * t.pmax; ++u) {
+          const int val = __ldg(mcol + (long long)min(max(vstart + u, 0), g.H - 1) * mrow);
+          const int au = u > t.pmax ? u - t.pmax : t.pmax - u;
+#pragma unroll
+          for (int i = 0; i < K; ++i)
+            if (au <= t.p[i]) box[i] += val;
+        }
+      }
+      while (out_next < b) {
+        const int nb = min(HB, b - out_next);
+        if (produced < (out_next - a) + nb + 2 * t.pmax + 1) break;
+        float ov[HB];
+#pragma unroll
+        for (int r = 0; r < HB; ++r) ov[r] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          uint32_t lv[HB], tv[HB];
+          tmem_ld16(tlane + (uint32_t)lead_s[i], lv);
+          // the trail of row out_next is still in the ring iff D >= 2*HB + pmax + p_i
+          const bool trail_in_ring = (2 * HB + t.pmax + t.p[i]) <= D;
+          if (trail_in_ring) tmem_ld16(tlane + (uint32_t)trail_s[i], tv);
+          tmem_wait_ld();
+          if (!trail_in_ring) load_band(out_next - t.p[i] - 1, tv);
+          int bx = box[i];
+          const float w = t.w_col[i];
+#pragma unroll
+          for (int r = 0; r < HB; ++r) {
+            bx += (int)lv[r] - (int)tv[r];
+            ov[r] = fmaf(w, (float)bx, ov[r]);
+          }
+          box[i] = bx;
+          lead_s[i] += HB;
+          lead_s[i] = lead_s[i] >= D ? lead_s[i] - D : lead_s[i];
+          trail_s[i] += HB;
+          trail_s[i] = trail_s[i] >= D ? trail_s[i] - D : trail_s[i];
+        }
+        if (active) {
+          float* dptr = dst + (long long)img * g.out_img + (long long)out_next * g.out_row +
+                        (long long)(x0 + c) * g.out_px + ch;
+          const long long step = g.out_row;
+#pragma unroll
+          for (int r = 0; r < HB; ++r) {
+            if (r < nb) st_stream(dptr, ov[r]);
+            dptr += step;
+          }
+        }
+        out_next += nb;
+      }
+    }
   }
+  tmem_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem_base_s, (uint32_t)tl.tmem_cols);
 }
 
 // ---------------------------------------------------------------- fused, warp-specialised
@@ -652,13 +682,14 @@ constexpr int NCONS = WS / 32;
 constexpr int NPROD = 2;
 constexpr int FUSED_THREADS = 32 * (NCONS + NPROD);
 constexpr int NSTAGE = 2 * NPROD;  // staged bands (each producer warp double-buffers its own)
+constexpr int NPBUF = 2 * NPROD;   // prefix buffers (each producer warp owns two)
 
 template <typename Tin, int K>
 __global__ void __launch_bounds__(FUSED_THREADS, 3)
     fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
-  __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2];
+  __shared__ __align__(8) uint64_t bar_full[NPBUF], bar_empty[NPBUF];
   const int strip = blockIdx.x % tl.nstrips;
   const long long item = blockIdx.x / tl.nstrips;
   const int ch = blockIdx.y;
@@ -672,14 +703,14 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
   const bool packed = (sizeof(Tin) == 1) && tl.packed;
   const int pbuf_words = packed ? (HB / 2) * LSP : HB * LS;
   unsigned char* stage = smem;                                       // 2 producers x 2 staged bands
-  int* Pbase = (int*)(smem + NSTAGE * HB * tl.stage_row_bytes);      // 2 prefix buffers
+  int* Pbase = (int*)(smem + NSTAGE * HB * tl.stage_row_bytes);      // NPBUF prefix buffers
   const int D = tl.D;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar_full[0], 32);  // one producer warp fills a prefix buffer
-    mbar_init(&bar_full[1], 32);
-    mbar_init(&bar_empty[0], 32 * NCONS);
-    mbar_init(&bar_empty[1], 32 * NCONS);
+    for (int i = 0; i < NPBUF; ++i) {
+      mbar_init(&bar_full[i], 32);  // one producer warp fills a prefix buffer
+      mbar_init(&bar_empty[i], 32 * NCONS);
+    }
   }
   if (warp == 0) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
   tmem_fence_before();
@@ -699,7 +730,6 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
     const int st_nchunk = max(0, (st_hi16 - st_lo) >> 4);
     const uint32_t st_magic = 0xFFFFFFFFu / (uint32_t)max(1, st_nchunk) + 1u;
     unsigned char* mystage = stage + pw * 2 * HB * tl.stage_row_bytes;
-    int* P = Pbase + pw * pbuf_words;
     uint32_t gb0 = 0;  // global index of the segment's first band
     for (long long T = T0; T < T1;) {
       const int img = (int)(T / g.H);
@@ -728,12 +758,17 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
           fixup_edges(cur, g, tl, xb, n, lane, 32);
           __syncwarp();
         }
-        mbar_wait(&bar_empty[pw], ((gb >> 1) & 1) ^ 1);  // consumers done with prefix buffer pw
+        // this producer's (gb >> 1)-th band -> its buffer (gb >> 1) % npb, used for the
+        // ((gb >> 1) / npb)-th time
+        const uint32_t kb = gb >> 1;
+        const int pbi = pw * tl.npb + (int)(kb % (uint32_t)tl.npb);
+        int* P = Pbase + pbi * pbuf_words;
+        mbar_wait(&bar_empty[pbi], ((kb / (uint32_t)tl.npb) & 1) ^ 1);  // consumers done with it
         if (packed)
           scan_rows_packed(cur, (uint32_t*)P, tl, 0, 1);
         else
           scan_rows<Tin>(cur, P, g, t, tl, ch, n, status, 0, 1);
-        mbar_arrive(&bar_full[pw]);
+        mbar_arrive(&bar_full[pbi]);
       }
       gb0 += (uint32_t)nbands;
     }
@@ -756,14 +791,16 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
       int out_next = a, out_mod = 0, prod_slot = 0;
       for (int pb = 0; pb < nbands; ++pb, ++gb) {
         const int n = min(HB, count - pb * HB);
-        const int* P = Pbase + (gb & 1) * pbuf_words;
+        const uint32_t kb = gb >> 1;
+        const int pbi = (int)(gb & 1) * tl.npb + (int)(kb % (uint32_t)tl.npb);
+        const int* P = Pbase + pbi * pbuf_words;
         float rv[HB];
-        mbar_wait(&bar_full[gb & 1], (gb >> 1) & 1);
+        mbar_wait(&bar_full[pbi], (kb / (uint32_t)tl.npb) & 1);
         if (packed)
           band_rows_packed<K>((const uint32_t*)P, c, t, tl, rv);
         else
           band_rows<K, LS>(P, c, t.w_row, t, tl, rv);
-        mbar_arrive(&bar_empty[gb & 1]);
+        mbar_arrive(&bar_empty[pbi]);
         {
           uint32_t bits[HB];
 #pragma unroll
@@ -833,6 +870,171 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
   if (warp == 0) tmem_dealloc(tmem_base_s, (uint32_t)tl.tmem_cols);
 }
 
+// ---------------------------------------------------------------- streaming row pass (large radii)
+// RowsToMid for radii too large for the fused sweep.  A CTA owns a band of HB
+// rows and streams its full width in chunks of CW columns, so the 2*pmax+1
+// halo is paid once per row instead of once per strip: producer warp pw stages
+// and prefix-scans rows 8pw..8pw+7 of each chunk (the row prefix carried across
+// chunks) into a ring of RL prefix columns; consumer thread c emits column
+// o*CW + c of output chunk o once the chunk holding its lead prefix is scanned.
+// Virtual column q = x - xs with xs = the first column of the left halo
+// (rounded down to 16 so cp.async stays aligned); columns outside [0, W)
+// replicate the border (filtering.py:10-13).
+constexpr int CW = 128;    // chunk width (= consumer threads)
+constexpr int RL = 1024;   // prefix ring length (power of two, >= 3*CW + 2*pmax + 2)
+
+constexpr int NSLOT = RL / CW;  // ring chunk slots; one full/done mbarrier per slot (no phase aliasing)
+
+template <typename Tin, int K>
+__global__ void __launch_bounds__(FUSED_THREADS, 2)
+    stream_rows_kernel(const Tin* __restrict__ src, int* __restrict__ mid_out, Geometry g, Taps t, int xs,
+                       int nbands_total, int* status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
+  __shared__ int carry_s[HB];
+  const int warp = threadIdx.x >> 5;
+  const bool producer = warp >= NCONS;
+  const int qtotal = g.W - xs + t.pmax;  // virtual columns q = x - xs, x in [xs, W + pmax)
+  const int nin = (qtotal + CW - 1) / CW;
+  const int nout = (g.W + CW - 1) / CW;
+  // output chunk o reads prefix columns of input chunks o .. o + lagc
+  const int lagc = (CW - 1 - xs + t.pmax) / CW;
+  const int rowbytes = CW * (int)sizeof(Tin);
+  unsigned char* stage = smem;                           // [NPROD][2][8][CW] elements
+  int* P = (int*)(smem + NPROD * 2 * 8 * rowbytes);      // [HB][RL]
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSLOT; ++i) {
+      mbar_init(&bar_full[i], 32 * NPROD);
+      mbar_init(&bar_done[i], 32 * NCONS);
+    }
+  }
+  __syncthreads();
+
+  const int ch = blockIdx.y;
+  uint32_t cin_ctr = 0, out_ctr = 0;  // input chunks / output chunks completed by this CTA
+  for (int band = blockIdx.x; band < nbands_total; band += gridDim.x) {
+    const long long row0 = (long long)band * HB;
+    const int nrows = (int)min((long long)HB, (long long)g.nimg * g.H - row0);
+    if (producer) {
+      const int lane = threadIdx.x & 31, pw = warp - NCONS;
+      unsigned char* mystage = stage + pw * 2 * 8 * rowbytes;
+      auto issue = [&](int j, int buf) {
+        const int xq0 = xs + j * CW;
+        for (int idx = lane; idx < 8 * CW; idx += 32) {
+          const int rr = idx / CW, e = idx - rr * CW;
+          const long long trow = row0 + min(8 * pw + rr, nrows - 1);
+          const int img = (int)(trow / g.H), v = (int)(trow - (long long)img * g.H);
+          const int x = min(max(xq0 + e, 0), g.W - 1);  // replicate border columns
+          const Tin* gp = src + (long long)img * g.in_img + (long long)v * g.in_row + (long long)x * g.in_px + ch;
+          Tin* sp = (Tin*)(mystage + (buf * 8 + rr) * rowbytes) + e;
+          if constexpr (sizeof(Tin) == 4) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(sp)), "l"(gp));
+          } else {
+            *sp = *gp;
+          }
+        }
+        cp_async_commit();
+      };
+      if (lane < 8) carry_s[8 * pw + lane] = 0;
+      __syncwarp();
+      issue(0, 0);
+      bool bad = false;
+      for (int j = 0; j < nin; ++j) {
+        const uint32_t gj = cin_ctr + j;
+        cp_async_wait_all();
+        __syncwarp();
+        if (j + 1 < nin) issue(j + 1, (j + 1) & 1);
+        if (j >= NSLOT) {  // ring slot of chunk j last served output chunk j - NSLOT
+          const uint32_t go = out_ctr + (j - NSLOT);
+          mbar_wait(&bar_done[go % NSLOT], (go / NSLOT) & 1);
+        }
+        const unsigned char* cur = mystage + (j & 1) * 8 * rowbytes;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          const int rr = pass * 4 + (lane >> 3), sc = lane & 7;
+          const Tin* e = (const Tin*)(cur + rr * rowbytes) + sc * CH;
+          int v[CH];
+          int tot = 0;
+#pragma unroll
+          for (int m = 0; m < CH; ++m) {
+            tot += to_fixed<Tin>(e[m], t, bad);
+            v[m] = tot;
+          }
+          int inc = tot;
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o, 8);
+            if (sc >= o) inc += y;
+          }
+          const int r = 8 * pw + rr;
+          const int cin = carry_s[r];
+          const int off = cin + inc - tot;
+          int* dst = P + r * RL + ((j * CW + sc * CH) & (RL - 1));
+#pragma unroll
+          for (int m = 0; m < CH / 4; ++m)
+            ((int4*)dst)[m] = make_int4(v[4 * m] + off, v[4 * m + 1] + off, v[4 * m + 2] + off, v[4 * m + 3] + off);
+          const int total_row = __shfl_sync(0xffffffffu, inc, 7, 8);
+          __syncwarp();
+          if (sc == 0) carry_s[r] = cin + total_row;
+          __syncwarp();
+        }
+        mbar_arrive(&bar_full[gj % NSLOT]);
+      }
+      if (bad && status) atomicOr(status, SB_STATUS_RANGE);
+    } else {
+      const int c = threadIdx.x;
+      for (int o = 0; o < nout; ++o) {
+        const uint32_t gj = cin_ctr + min(o + lagc, nin - 1);  // chunks complete in order
+        mbar_wait(&bar_full[gj % NSLOT], (gj / NSLOT) & 1);
+        const int x = o * CW + c;
+        float rv[HB];
+#pragma unroll
+        for (int r = 0; r < HB; ++r) rv[r] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          const int* pl = P + ((x - xs + t.p[i]) & (RL - 1));
+          const int* pt = P + ((x - xs - t.p[i] - 1) & (RL - 1));
+          const float wi = t.w_row[i];
+#pragma unroll
+          for (int r = 0; r < HB; ++r) rv[r] = fmaf(wi, (float)(pl[r * RL] - pt[r * RL]), rv[r]);
+        }
+        const uint32_t go = out_ctr + o;
+        mbar_arrive(&bar_done[go % NSLOT]);
+        if (x < g.W) {
+#pragma unroll
+          for (int r = 0; r < HB; ++r) {
+            if (r < nrows) {
+              const long long trow = row0 + r;
+              const int img = (int)(trow / g.H), v = (int)(trow - (long long)img * g.H);
+              mid_out[ch * g.mid_ch + (long long)img * g.mid_img + (long long)v * g.mid_row + x] =
+                  __float_as_int(rv[r] + kMagic) - kMagicBits;
+            }
+          }
+        }
+      }
+    }
+    cin_ctr += (uint32_t)nin;
+    out_ctr += (uint32_t)nout;
+    __syncthreads();  // the next band restarts the ring and the carries
+  }
+}
+
+inline const void* stream_ptr_for_f32(int k) {
+#define SB_STREAM(KK) stream_rows_kernel<float, KK>
+  switch (k) {
+    case 1: return (const void*)SB_STREAM(1);
+    case 2: return (const void*)SB_STREAM(2);
+    case 3: return (const void*)SB_STREAM(3);
+    case 4: return (const void*)SB_STREAM(4);
+    case 5: return (const void*)SB_STREAM(5);
+    case 6: return (const void*)SB_STREAM(6);
+    case 7: return (const void*)SB_STREAM(7);
+    default: return (const void*)SB_STREAM(8);
+  }
+#undef SB_STREAM
+}
+
 // Kernel pointers per source type, instantiated in sweep_<dtype>.cu (one
 // translation unit each, compiled in parallel).
 const void* sweep_ptr_u8(Mode m, int k);
@@ -840,38 +1042,40 @@ const void* sweep_ptr_u16(Mode m, int k);
 const void* sweep_ptr_f32(Mode m, int k);
 const void* sweep_ptr_f64(Mode m, int k);
 const void* sweep_ptr_cols(int k);  // ColsFromMid (source type unused)
+const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)
 
 template <typename Tin>
 const void* sweep_ptr_for(Mode m, int k) {
-#define SB_K_CASES(MODE)                                         \
-  switch (k) {                                                   \
-    case 1: return (const void*)sweep_kernel<Tin, 1, MODE>;      \
-    case 2: return (const void*)sweep_kernel<Tin, 2, MODE>;      \
-    case 3: return (const void*)sweep_kernel<Tin, 3, MODE>;      \
-    case 4: return (const void*)sweep_kernel<Tin, 4, MODE>;      \
-    case 5: return (const void*)sweep_kernel<Tin, 5, MODE>;      \
-    case 6: return (const void*)sweep_kernel<Tin, 6, MODE>;      \
-    case 7: return (const void*)sweep_kernel<Tin, 7, MODE>;      \
-    default: return (const void*)sweep_kernel<Tin, 8, MODE>;     \
+#define SB_K_CASES(KERNEL)                                 \
+  switch (k) {                                             \
+    case 1: return (const void*)KERNEL(1);                 \
+    case 2: return (const void*)KERNEL(2);                 \
+    case 3: return (const void*)KERNEL(3);                 \
+    case 4: return (const void*)KERNEL(4);                 \
+    case 5: return (const void*)KERNEL(5);                 \
+    case 6: return (const void*)KERNEL(6);                 \
+    case 7: return (const void*)KERNEL(7);                 \
+    default: return (const void*)KERNEL(8);                \
   }
-  if (m == Mode::Fused) {
-    switch (k) {
-      case 1: return (const void*)fused_kernel<Tin, 1>;
-      case 2: return (const void*)fused_kernel<Tin, 2>;
-      case 3: return (const void*)fused_kernel<Tin, 3>;
-      case 4: return (const void*)fused_kernel<Tin, 4>;
-      case 5: return (const void*)fused_kernel<Tin, 5>;
-      case 6: return (const void*)fused_kernel<Tin, 6>;
-      case 7: return (const void*)fused_kernel<Tin, 7>;
-      default: return (const void*)fused_kernel<Tin, 8>;
-    }
-  }
+#define SB_FUSED(KK) fused_kernel<Tin, KK>
+#define SB_ROWS_MID(KK) rows_kernel<Tin, KK, Mode::RowsToMid>
+#define SB_ROWS_OUT(KK) rows_kernel<Tin, KK, Mode::RowsToOut>
   switch (m) {
-    case Mode::RowsToMid: SB_K_CASES(Mode::RowsToMid)
-    case Mode::RowsToOut: SB_K_CASES(Mode::RowsToOut)
+    case Mode::Fused: SB_K_CASES(SB_FUSED)
+    case Mode::RowsToMid: SB_K_CASES(SB_ROWS_MID)
+    case Mode::RowsToOut: SB_K_CASES(SB_ROWS_OUT)
     default: break;
   }
   return nullptr;
+#undef SB_FUSED
+#undef SB_ROWS_MID
+#undef SB_ROWS_OUT
+}
+
+inline const void* cols_ptr_for(int k) {
+#define SB_COLS(KK) cols_kernel<KK>
+  SB_K_CASES(SB_COLS)
+#undef SB_COLS
 #undef SB_K_CASES
 }
 

@@ -193,7 +193,7 @@ def separable_filter_batch(images, kernel: SliceKernel, *, channels_last: bool =
         result = torch.empty(tuple(dev.tensor.shape), dtype=torch.float32, device=x.device)
     radii, weights, rp, wp = _kernel_arrays(kernel)
     lib = nat.load()
-    ws_bytes = lib.sb_separable_filter_2d_workspace_bytes(b, h, w, c, rp, kernel.k)
+    ws_bytes = lib.sb_separable_filter_2d_workspace_bytes(dev.code, b, h, w, c, rp, kernel.k)
     workspace = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=x.device)
     status = torch.zeros(1, dtype=torch.int32, device=x.device)
     bound = dev.value_bound(value_bound)

@@ -37,7 +37,7 @@ def test_exports_every_header_symbol(lib):
     assert set(syms) == set(nat.EXPORTED_SYMBOLS)
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.sb_version() == 1
+    assert lib.sb_version() == 2
 
 
 def _k(radii, weights):
@@ -89,9 +89,9 @@ def test_invalid_arguments_fail_before_cuda(lib):
 def test_workspace_sizes(lib):
     small = A.table_kernel(3, 10.0)  # pmax 23 -> fused, no workspace
     r, w, rp, wp = _k(small.radii, small.weights)
-    assert lib.sb_separable_filter_2d_workspace_bytes(256, 1024, 1024, 1, rp, 3) == 0
+    assert lib.sb_separable_filter_2d_workspace_bytes(nat.SB_DTYPE_U8, 256, 1024, 1024, 1, rp, 3) == 0
     big = A.table_kernel(4, 100.0)  # pmax 257 -> two launches through an int32 plane
     r, w, rp, wp = _k(big.radii, big.weights)
-    assert lib.sb_separable_filter_2d_workspace_bytes(1, 1000, 2000, 3, rp, 4) == 1000 * 2000 * 3 * 4
+    assert lib.sb_separable_filter_2d_workspace_bytes(nat.SB_DTYPE_F32, 1, 1000, 2000, 3, rp, 4) == 1000 * 2000 * 3 * 4
     assert lib.sb_prefix_sum_workspace_bytes(1) == 8
     assert lib.sb_prefix_sum_workspace_bytes(2048 * 3 + 1) == 4 * 8
