@@ -156,17 +156,19 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
   return tl;
 }
 
+// Dynamic shared memory that limits residency to `ctas` CTAs per SM (the TMEM
+// ring kernels must never have a CTA waiting inside tcgen05.alloc).
+size_t residency_floor(int ctas) { return 233472 / (size_t)(ctas + 1) - 1024 + 16; }
+
 size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
-  if (m == sb::Mode::ColsFromMid) return 0;
+  if (m == sb::Mode::ColsFromMid) return residency_floor(512 / tl.tmem_cols);
   if (m == sb::Mode::Fused) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
     const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP * sizeof(int) : (size_t)sb::HB * sb::LS * sizeof(int);
     size_t s = (size_t)sb::NSTAGE * sb::HB * tl.stage_row_bytes + (size_t)sb::NPROD * tl.npb * pbuf;
     // cap residency at 512 / tmem_cols CTAs per SM by asking for enough shared
     // memory, so no CTA ever waits inside tcgen05.alloc
-    const int ctas = 512 / tl.tmem_cols;
-    const size_t floor_bytes = 233472 / (size_t)(ctas + 1) - 1024 + 16;
-    return std::max(s, floor_bytes);
+    return std::max(s, residency_floor(512 / tl.tmem_cols));
   }
   return (size_t)2 * sb::HB * tl.stage_row_bytes + (size_t)sb::HB * tl.ls * sizeof(int);
 }
