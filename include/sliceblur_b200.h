@@ -10,6 +10,7 @@
  *
  *   sb_check_kernel          <- filtering.py:39-45   _check_kernel
  *   sb_separable_filter_2d   <- filtering.py:76-104  separable_filter_2d
+ *   sb_separable_filter_2d_window  (row-strip variant for the multi-GPU partition)
  *                               (+ batched / interleaved-channel layouts that
  *                               the reference reaches by looping in Python)
  *   sb_slice_filter_1d       <- filtering.py:67-73   slice_filter_1d
@@ -91,6 +92,20 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
                            int64_t dst_image_stride, int64_t dst_row_stride, const int64_t* radii,
                            const double* weights, int k, double value_bound, void* workspace,
                            size_t workspace_bytes, int* status_dev, void* stream);
+
+/* Strip variant of sb_separable_filter_2d (the multi-GPU row-strip partition):
+ * `src` holds `height` rows per image - a strip plus the halo rows received
+ * from its neighbours - and only output rows [row_begin, row_end) are
+ * written, to dst rows 0 .. row_end-row_begin-1.  Rows outside [0, height)
+ * replicate the first/last row, so a strip at the global top/bottom passes
+ * no halo there and gets the reference's boundary; interior strip edges see
+ * real neighbour rows (a halo of radii[k-1] rows suffices). */
+int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch, int64_t height, int64_t width,
+                                  int channels, int64_t src_image_stride, int64_t src_row_stride,
+                                  int64_t row_begin, int64_t row_end, float* dst, int64_t dst_image_stride,
+                                  int64_t dst_row_stride, const int64_t* radii, const double* weights, int k,
+                                  double value_bound, void* workspace, size_t workspace_bytes, int* status_dev,
+                                  void* stream);
 
 /* filtering.py:48-64 _filter_rows: the row pass alone, every row of a
  * (rows x width) array (row stride in elements), float32 output. */

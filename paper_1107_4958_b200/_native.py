@@ -35,6 +35,7 @@ EXPORTED_SYMBOLS = (
     "sb_check_kernel",
     "sb_separable_filter_2d_workspace_bytes",
     "sb_separable_filter_2d",
+    "sb_separable_filter_2d_window",
     "sb_filter_rows",
     "sb_slice_filter_1d",
     "sb_prefix_sum_workspace_bytes",
@@ -73,6 +74,14 @@ def _declare(lib):
         _vp, _size, _vp, _vp,  # workspace, bytes, status, stream
     ]
     lib.sb_separable_filter_2d.restype = _int
+    lib.sb_separable_filter_2d_window.argtypes = [
+        _vp, _int, _i64, _i64, _i64, _int, _i64, _i64,  # src, dtype, batch, h, w, channels, img/row stride
+        _i64, _i64,  # row_begin, row_end
+        _vp, _i64, _i64,  # dst, img/row stride
+        _i64p, _f64p, _int, ctypes.c_double,
+        _vp, _size, _vp, _vp,
+    ]
+    lib.sb_separable_filter_2d_window.restype = _int
     lib.sb_filter_rows.argtypes = [_vp, _int, _i64, _i64, _i64, _vp, _i64, _i64p, _f64p, _int, ctypes.c_double, _vp,
                                    _vp]
     lib.sb_filter_rows.restype = _int

@@ -308,19 +308,23 @@ size_t sb_separable_filter_2d_workspace_bytes(int src_dtype, int64_t batch, int6
   return (size_t)batch * height * width * channels * sizeof(int);
 }
 
-int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_t height, int64_t width,
-                           int channels, int64_t src_image_stride, int64_t src_row_stride, float* dst,
-                           int64_t dst_image_stride, int64_t dst_row_stride, const int64_t* radii,
-                           const double* weights, int k, double value_bound, void* workspace,
-                           size_t workspace_bytes, int* status_dev, void* stream) {
+int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch, int64_t height, int64_t width,
+                                  int channels, int64_t src_image_stride, int64_t src_row_stride,
+                                  int64_t row_begin, int64_t row_end, float* dst, int64_t dst_image_stride,
+                                  int64_t dst_row_stride, const int64_t* radii, const double* weights, int k,
+                                  double value_bound, void* workspace, size_t workspace_bytes, int* status_dev,
+                                  void* stream) {
+  if (row_begin < 0 || row_end > height || row_begin >= row_end)
+    return fail(SB_ERR_INVALID_ARGUMENT, "need 0 <= row_begin < row_end <= height");
   if (!src || !dst) return fail(SB_ERR_INVALID_ARGUMENT, "src/dst must not be NULL");
   if (batch < 1 || height < 1 || width < 1) return fail(SB_ERR_INVALID_ARGUMENT, "need a non-empty 2D image");
   if (channels < 1) return fail(SB_ERR_INVALID_ARGUMENT, "channels must be >= 1");
   if (height > 0x7fffffff || width > 0x7fffffff) return fail(SB_ERR_INVALID_ARGUMENT, "extent exceeds int32");
   if (src_row_stride < width * channels || dst_row_stride < width * channels)
     return fail(SB_ERR_INVALID_ARGUMENT, "row stride smaller than width * channels");
-  if (batch > 1 && (src_image_stride < height * src_row_stride || dst_image_stride < height * dst_row_stride))
-    return fail(SB_ERR_INVALID_ARGUMENT, "image stride smaller than height * row stride");
+  if (batch > 1 && (src_image_stride < height * src_row_stride ||
+                    dst_image_stride < (row_end - row_begin) * dst_row_stride))
+    return fail(SB_ERR_INVALID_ARGUMENT, "image stride smaller than rows * row stride");
   int rc = sb_check_kernel(radii, weights, k, width);
   if (rc) return rc;
   rc = sb_check_kernel(radii, weights, k, height);
@@ -342,9 +346,12 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
   g.H = (int)height;
   g.W = (int)width;
   g.nimg = (int)batch;
+  g.oy0 = (int)row_begin;
+  g.oy1 = (int)row_end;
   g.aligned16 = ((uintptr_t)src % 16 == 0) && ((src_row_stride * g.es) % 16 == 0) &&
                 (batch == 1 || (src_image_stride * g.es) % 16 == 0);
-  const long long total_rows = (long long)batch * height;
+  const long long total_rows = (long long)batch * (row_end - row_begin);  // rows the column sweep outputs
+  const long long all_rows = (long long)batch * height;                   // rows the row pass produces
   const bool u8_single = (src_dtype == SB_DTYPE_U8 && channels == 1);
   const sb::Tiling base = make_tiling(sb::Mode::Fused, plan.pmax, channels, g.es, u8_single);
 
@@ -374,7 +381,7 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int nb_total = (int)((total_rows + sb::HB - 1) / sb::HB);
+    const int nb_total = (int)((all_rows + sb::HB - 1) / sb::HB);
     const int gx = std::max(1, std::min(nb_total, sms * 2 * 8 / std::max(1, channels)));
     void* args[] = {(void*)&src, (void*)&mid, (void*)&g, (void*)&plan.taps, (void*)&xs, (void*)&nb_total,
                     (void*)&status_dev};
@@ -387,7 +394,7 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
   const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);
   Launch L1;
   rc = plan_launch(f1, sb::Mode::RowsToMid, make_tiling(sb::Mode::RowsToMid, plan.pmax, channels, g.es, false),
-                   plan.pmax, g.W, total_rows, channels, &L1);
+                   plan.pmax, g.W, all_rows, channels, &L1);
   if (rc) return rc;
   rc = launch_rows(f1, L1, src, mid, nullptr, g, plan.taps, status_dev, st);
   if (rc) return rc;
@@ -398,6 +405,17 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
                    plan.pmax, g.W, total_rows, channels, &L2);
   if (rc) return rc;
   return launch_cols(f2, L2, mid, dst, g, plan.taps, st);
+}
+
+int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_t height, int64_t width,
+                           int channels, int64_t src_image_stride, int64_t src_row_stride, float* dst,
+                           int64_t dst_image_stride, int64_t dst_row_stride, const int64_t* radii,
+                           const double* weights, int k, double value_bound, void* workspace,
+                           size_t workspace_bytes, int* status_dev, void* stream) {
+  if (height < 1) return fail(SB_ERR_INVALID_ARGUMENT, "need a non-empty 2D image");
+  return sb_separable_filter_2d_window(src, src_dtype, batch, height, width, channels, src_image_stride,
+                                       src_row_stride, 0, height, dst, dst_image_stride, dst_row_stride, radii,
+                                       weights, k, value_bound, workspace, workspace_bytes, status_dev, stream);
 }
 
 int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, int64_t src_row_stride, float* dst,

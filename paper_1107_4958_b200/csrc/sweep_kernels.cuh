@@ -59,6 +59,7 @@ struct Geometry {
   long long mid_img, mid_row;  // int32 workspace strides (two-pass only)
   long long mid_ch;            // int32 workspace channel-plane stride
   int H, W, nimg;
+  int oy0, oy1;                // output row window of every image (column sweeps write rows oy0..oy1-1)
   int aligned16;               // rows are 16-byte aligned: cp.async 16 B staging
 };
 
@@ -559,7 +560,8 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
   const int c = threadIdx.x;
   const bool active = (x0 + c) < g.W;
   const int xc = active ? x0 + c : g.W - 1;  // inactive lanes mirror a valid column (no stores)
-  const long long total = (long long)g.nimg * g.H;
+  const int wh = g.oy1 - g.oy0;  // rows of each image this launch outputs
+  const long long total = (long long)g.nimg * wh;
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const int D = tl.D;
@@ -570,10 +572,10 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
   const uint32_t tlane = tmem_base_s + ((uint32_t)(threadIdx.x & ~31) << 16);
 
   for (long long T = T0; T < T1;) {
-    const int img = (int)(T / g.H);
-    const int a = (int)(T - (long long)img * g.H);
-    const int b = (int)min((long long)g.H, T1 - (long long)img * g.H);
-    T = (long long)img * g.H + b;
+    const int img = (int)(T / wh);
+    const int a = g.oy0 + (int)(T - (long long)img * wh);
+    const int b = g.oy0 + (int)min((long long)wh, T1 - (long long)img * wh);
+    T = (long long)img * wh + (b - g.oy0);
     const int* mcol = mid_in + ch * g.mid_ch + (long long)img * g.mid_img + xc;
     const long long mrow = g.mid_row;
     // rows of one band, clamped only where the band crosses the image top or bottom
@@ -657,7 +659,7 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
           trail_s[i] = trail_s[i] >= D ? trail_s[i] - D : trail_s[i];
         }
         if (active) {
-          float* dptr = dst + (long long)img * g.out_img + (long long)out_next * g.out_row +
+          float* dptr = dst + (long long)img * g.out_img + (long long)(out_next - g.oy0) * g.out_row +
                         (long long)(x0 + c) * g.out_px + ch;
           const long long step = g.out_row;
 #pragma unroll
@@ -702,7 +704,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
   const int xb = x0 - tl.xoff;
   const int warp = threadIdx.x >> 5;
   const bool producer = warp >= NCONS;
-  const long long total = (long long)g.nimg * g.H;
+  const int wh = g.oy1 - g.oy0;  // rows of each image this launch outputs
+  const long long total = (long long)g.nimg * wh;
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const bool packed = (sizeof(Tin) == 1) && tl.packed;
@@ -737,10 +740,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
     unsigned char* mystage = stage + pw * 2 * HB * tl.stage_row_bytes;
     uint32_t gb0 = 0;  // global index of the segment's first band
     for (long long T = T0; T < T1;) {
-      const int img = (int)(T / g.H);
-      const int a = (int)(T - (long long)img * g.H);
-      const int b = (int)min((long long)g.H, T1 - (long long)img * g.H);
-      T = (long long)img * g.H + b;
+      const int img = (int)(T / wh);
+      const int a = g.oy0 + (int)(T - (long long)img * wh);
+      const int b = g.oy0 + (int)min((long long)wh, T1 - (long long)img * wh);
+      T = (long long)img * wh + (b - g.oy0);
       const Tin* src_img = src + (long long)img * g.in_img;
       const int vstart = a - 1 - t.pmax;
       const int count = (b - a) + 2 * t.pmax + 1;
@@ -784,10 +787,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
     const uint32_t tlane = tmem_base_s + ((uint32_t)(threadIdx.x & ~31) << 16);
     uint32_t gb = 0;
     for (long long T = T0; T < T1;) {
-      const int img = (int)(T / g.H);
-      const int a = (int)(T - (long long)img * g.H);
-      const int b = (int)min((long long)g.H, T1 - (long long)img * g.H);
-      T = (long long)img * g.H + b;
+      const int img = (int)(T / wh);
+      const int a = g.oy0 + (int)(T - (long long)img * wh);
+      const int b = g.oy0 + (int)min((long long)wh, T1 - (long long)img * wh);
+      T = (long long)img * wh + (b - g.oy0);
       const int count = (b - a) + 2 * t.pmax + 1;
       const int nbands = (count + HB - 1) / HB;
       int box[K];
@@ -846,7 +849,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
           float ov[HB];
           column_band_tmem<K>(tlane, lead_s, trail_s, box, t, ov);
           if (active) {
-            float* dptr = dst + (long long)img * g.out_img + (long long)out_next * g.out_row +
+            float* dptr = dst + (long long)img * g.out_img + (long long)(out_next - g.oy0) * g.out_row +
                           (long long)(x0 + c) * g.out_px + ch;
             const long long step = g.out_row;
             if (nb == HB) {

@@ -29,6 +29,7 @@ from .approx import SliceKernel
 
 __all__ = [
     "KernelTooLargeError",
+    "separable_filter_window",
     "filter_rows",
     "prefix_sum",
     "separable_filter_2d",
@@ -205,6 +206,50 @@ def separable_filter_batch(images, kernel: SliceKernel, *, channels_last: bool =
     )
     _raise_for(code)
     return dev.finish(result, status, check, host_out)
+
+
+def separable_filter_window(image, kernel: SliceKernel, row_begin: int, row_end: int, *, channels_last: bool = False,
+                            value_bound=None, out=None, check: bool = True):
+    """Rows [row_begin, row_end) of ``separable_filter_2d(image)`` (strip variant).
+
+    ``image`` is (H, W) or, with ``channels_last``, (H, W, C).  Used by the
+    row-strip partition (``distributed.filter_strip``): the image is a strip
+    plus its neighbours' halo rows, and only the strip's own rows are output.
+    Returns (row_end - row_begin, W[, C]) float32.
+    """
+    dev = _Device(image)
+    x = dev.tensor
+    if channels_last:
+        if x.dim() != 3:
+            raise ValueError("channels_last input must be (H, W, C)")
+        h, w, c = x.shape
+    else:
+        if x.dim() != 2:
+            raise ValueError("need a 2D image")
+        h, w = x.shape
+        c = 1
+    if min(h, w, c) < 1:
+        raise ValueError("need a non-empty 2D image")
+    if not 0 <= row_begin < row_end <= h:
+        raise ValueError("need 0 <= row_begin < row_end <= height")
+    _check_kernel(kernel, w)
+    _check_kernel(kernel, h)
+    torch = dev.torch
+    shape = (row_end - row_begin, w) + ((c,) if channels_last else ())
+    result = out if out is not None else torch.empty(shape, dtype=torch.float32, device=x.device)
+    if result.dtype != torch.float32 or not result.is_cuda or not result.is_contiguous() or tuple(result.shape) != shape:
+        raise ValueError("out must be a contiguous float32 CUDA tensor of shape %r" % (shape,))
+    radii, weights, rp, wp = _kernel_arrays(kernel)
+    lib = nat.load()
+    ws_bytes = lib.sb_separable_filter_2d_workspace_bytes(dev.code, 1, h, w, c, rp, kernel.k)
+    workspace = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=x.device)
+    status = torch.zeros(1, dtype=torch.int32, device=x.device)
+    bound = dev.value_bound(value_bound)
+    _raise_for(lib.sb_separable_filter_2d_window(
+        x.data_ptr(), dev.code, 1, h, w, c, h * w * c, w * c, row_begin, row_end,
+        result.data_ptr(), (row_end - row_begin) * w * c, w * c,
+        rp, wp, kernel.k, bound, workspace.data_ptr(), int(ws_bytes), status.data_ptr(), dev.stream))
+    return dev.finish(result, status, check)
 
 
 def separable_filter_2d(image, kernel: SliceKernel, parallel: bool = False, *, value_bound=None, out=None,

@@ -214,3 +214,27 @@ def test_torch_tensor_in_out_and_u16():
     got = F.separable_filter_2d(u16, kern)
     ref = O.separable_filter_2d(u16, kern.radii, kern.weights)
     assert np.abs(got - ref).max() <= BAR * 65535 / 255
+
+
+@pytest.mark.parametrize("k,sigma", [(3, 4.0), (4, 40.0)])  # fused sweep, then the two-launch path
+def test_row_window_strips_match_full_image(k, sigma):
+    # the multi-GPU row-strip partition, emulated on one GPU: each "rank" filters its
+    # strip plus pmax halo rows with the row-window entry point
+    from paper_1107_4958_b200 import distributed as D
+
+    rng = np.random.default_rng(11)
+    img = (rng.random((600, 500)) * 255).astype(np.float32)
+    kern = A.table_kernel(k, sigma)
+    full = F.separable_filter_2d(img, kern, value_bound=255.0)
+    pmax = kern.max_radius
+    for world in (2, 3):
+        parts = []
+        for rank in range(world):
+            r0, r1 = D.shard_range(img.shape[0], rank, world)
+            top = pmax if rank > 0 else 0
+            bottom = pmax if rank < world - 1 else 0
+            ext = img[r0 - top:r1 + bottom]
+            parts.append(F.separable_filter_window(ext, kern, top, top + (r1 - r0), value_bound=255.0))
+        np.testing.assert_array_equal(np.concatenate(parts), full)
+    ref = O.separable_filter_2d(img, kern.radii, kern.weights, threads=THREADS)
+    assert np.abs(full - ref).max() <= BAR
