@@ -149,7 +149,12 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
   tl.packed = (m == sb::Mode::Fused && u8_single && nchunk <= 32 && tl.L <= sb::LSP) ? 1 : 0;  // exact 16-bit prefixes
   tl.npb = tl.packed ? 2 : 1;  // unpacked prefix buffers are large: one per producer
   tl.D = ((2 * pmax + 2 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;  // multiple of HB
-  if (m == sb::Mode::ColsFromMid) tl.D = std::min(tl.D, 512 - sb::HB);  // deeper trails come from the plane
+  if (m == sb::Mode::ColsFromMid) {
+    // a shallow ring (128 TMEM columns: 4 CTAs per SM) measured fastest; trails deeper than the
+    // ring are re-read from the plane, kept in L2 by the evict_last policy of the first read
+    const char* cap = std::getenv("SB_COLS_RING");
+    tl.D = std::min(tl.D, (cap ? std::atoi(cap) : 128) - sb::HB);
+  }
   int cols = 32;
   while (cols < tl.D + sb::HB) cols <<= 1;
   tl.tmem_cols = cols;
@@ -266,7 +271,8 @@ int launch_rows(const void* fn, const Launch& L, const void* src, int* mid_out, 
 int launch_cols(const void* fn, const Launch& L, const int* mid_in, float* dst, const sb::Geometry& g,
                 const sb::Taps& t, cudaStream_t stream) {
   void* args[] = {(void*)&mid_in, (void*)&dst, (void*)&g, (void*)&t, (void*)&L.tl};
-  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::WS), args, L.smem, stream);
+  // channels are folded into grid.x (fastest varying), see cols_kernel
+  cudaError_t e = cudaLaunchKernel(fn, dim3(L.grid.x * L.grid.y), dim3(sb::WS), args, L.smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   return SB_OK;
 }
@@ -388,7 +394,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     if (std::getenv("SB_DEBUG"))
       std::fprintf(stderr, "[sliceblur_b200] stream rows: pmax=%d xs=%d lagc=%d bands=%d grid=%d x %d smem=%zu\n",
                    plan.pmax, xs, lagc, nb_total, gx, channels, smem);
-    e = cudaLaunchKernel(fs, dim3(gx, channels), dim3(sb::FUSED_THREADS), args, smem, st);
+    e = cudaLaunchKernel(fs, dim3(gx * channels, 1), dim3(sb::FUSED_THREADS), args, smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   } else {
   const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);

@@ -101,6 +101,17 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+// R-plane loads: keep the line in L2 (its row is re-read as a deep trail 2*pmax+1 rows later)
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int ld_keep(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ void st_stream(float* p, float v) {
   asm volatile("st.global.cs.f32 [%0], %1;\n" ::"l"(p), "f"(v));
 }
@@ -553,9 +564,12 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
   extern __shared__ __align__(16) unsigned char smem_floor[];  // residency cap only (see residency_floor)
   (void)smem_floor;
   __shared__ uint32_t tmem_base_s;
-  const int strip = blockIdx.x % tl.nstrips;
-  const long long item = blockIdx.x / tl.nstrips;
-  const int ch = blockIdx.y;
+  // channel varies fastest across CTAs: the channels of one pixel range run together and
+  // share the interleaved lines in L2 (reads and partial-sector writes merge there)
+  const int ch = blockIdx.x % g.in_px;
+  const int sidx = blockIdx.x / g.in_px;
+  const int strip = sidx % tl.nstrips;
+  const long long item = sidx / tl.nstrips;
   const int x0 = strip * WS;
   const int c = threadIdx.x;
   const bool active = (x0 + c) < g.W;
@@ -578,18 +592,20 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
     T = (long long)img * wh + (b - g.oy0);
     const int* mcol = mid_in + ch * g.mid_ch + (long long)img * g.mid_img + xc;
     const long long mrow = g.mid_row;
+    const uint64_t keep = l2_keep_policy();
     // rows of one band, clamped only where the band crosses the image top or bottom
     auto load_band = [&](int v0, uint32_t (&dst_)[HB]) {
       if (v0 >= 0 && v0 + HB <= g.H) {
         const int* p = mcol + (long long)v0 * mrow;
 #pragma unroll
         for (int r = 0; r < HB; ++r) {
-          dst_[r] = (uint32_t)__ldg(p);
+          dst_[r] = (uint32_t)ld_keep(p, keep);
           p += mrow;
         }
       } else {
 #pragma unroll
-        for (int r = 0; r < HB; ++r) dst_[r] = (uint32_t)__ldg(mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
+        for (int r = 0; r < HB; ++r)
+          dst_[r] = (uint32_t)ld_keep(mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow, keep);
       }
     };
     const int vstart = a - 1 - t.pmax;
@@ -607,14 +623,18 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
       trail_s[i] = (t.pmax - t.p[i]) % D;
     }
     int out_next = a, prod_slot = 0;
-    uint32_t nxt[HB];
+    uint32_t nxt[HB], nxt2[HB];  // two bands of look-ahead: loads overlap two bands of compute
     load_band(vstart, nxt);
+    if (nbands > 1) load_band(vstart + HB, nxt2);
     for (int pb = 0; pb < nbands; ++pb) {
       const int n = min(HB, count - pb * HB);
       uint32_t cur[HB];
 #pragma unroll
-      for (int r = 0; r < HB; ++r) cur[r] = nxt[r];
-      if (pb + 1 < nbands) load_band(vstart + (pb + 1) * HB, nxt);
+      for (int r = 0; r < HB; ++r) {
+        cur[r] = nxt[r];
+        nxt[r] = nxt2[r];
+      }
+      if (pb + 2 < nbands) load_band(vstart + (pb + 2) * HB, nxt2);
       tmem_st16(tlane + (uint32_t)prod_slot, cur);
       if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, cur);
       tmem_wait_st();
@@ -919,9 +939,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
   }
   __syncthreads();
 
-  const int ch = blockIdx.y;
-  uint32_t cin_ctr = 0, out_ctr = 0;  // input chunks / output chunks completed by this CTA
-  for (int band = blockIdx.x; band < nbands_total; band += gridDim.x) {
+  const int ch = blockIdx.x % g.in_px;  // channel fastest (see cols_kernel)
+  uint32_t cin_ctr = 0, out_ctr = 0;    // input chunks / output chunks completed by this CTA
+  const int nblk = gridDim.x / g.in_px;
+  for (int band = blockIdx.x / g.in_px; band < nbands_total; band += nblk) {
     const long long row0 = (long long)band * HB;
     const int nrows = (int)min((long long)HB, (long long)g.nimg * g.H - row0);
     if (producer) {
