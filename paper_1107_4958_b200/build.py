@@ -59,7 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     objdir = os.path.join(PKG, "build_obj")
     os.makedirs(objdir, exist_ok=True)
-    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + os.environ.get("SB_NVCC_EXTRA", "").split()
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")

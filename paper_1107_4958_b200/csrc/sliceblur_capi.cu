@@ -124,7 +124,7 @@ struct Launch {
 
 // Tiling of a strip sweep (see sweep_kernels.cuh): staged/prefix row [xb, xb+L)
 // with xb = x0 - xoff for a strip of `sw` columns; ring of D rows (+ HB mirror).
-sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_single) {
+sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_single, int pmin = 0) {
   sb::Tiling tl;
   std::memset(&tl, 0, sizeof(tl));
   tl.xoff = ceil16(pmax + 1);
@@ -150,10 +150,14 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
   tl.npb = tl.packed ? 2 : 1;  // unpacked prefix buffers are large: one per producer
   tl.D = ((2 * pmax + 2 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;  // multiple of HB
   if (m == sb::Mode::ColsFromMid) {
-    // a shallow ring (128 TMEM columns: 4 CTAs per SM) measured fastest; trails deeper than the
-    // ring are re-read from the plane, kept in L2 by the evict_last policy of the first read
-    const char* cap = std::getenv("SB_COLS_RING");
-    tl.D = std::min(tl.D, (cap ? std::atoi(cap) : 128) - sb::HB);
+    // The ring must hold every LEAD window: lag <= pmax - pmin + 3*HB behind the newest row.
+    // Trails deeper than the ring are re-read from the plane (kept in L2 by evict_last).
+    // Prefer a 256-column allocation (two CTAs per SM) when the leads fit in it.
+    const int d_full = tl.D;
+    const int d_lead = ((pmax - pmin + 3 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;
+    if (d_full + sb::HB <= 256) tl.D = d_full;
+    else if (d_lead + sb::HB <= 256) tl.D = 256 - sb::HB;
+    else tl.D = std::min(d_full, 512 - sb::HB);
   }
   int cols = 32;
   while (cols < tl.D + sb::HB) cols <<= 1;
@@ -407,7 +411,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
   }
   const void* f2 = pick_kernel(sb::Mode::ColsFromMid, src_dtype, k);
   Launch L2;
-  rc = plan_launch(f2, sb::Mode::ColsFromMid, make_tiling(sb::Mode::ColsFromMid, plan.pmax, channels, 4, false),
+  rc = plan_launch(f2, sb::Mode::ColsFromMid, make_tiling(sb::Mode::ColsFromMid, plan.pmax, channels, 4, false, (int)radii[0]),
                    plan.pmax, g.W, total_rows, channels, &L2);
   if (rc) return rc;
   return launch_cols(f2, L2, mid, dst, g, plan.taps, st);
