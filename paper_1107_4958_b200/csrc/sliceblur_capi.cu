@@ -174,7 +174,7 @@ size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
   if (m == sb::Mode::Fused) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
     const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP * sizeof(int) : (size_t)sb::HB * sb::LS * sizeof(int);
-    size_t s = (size_t)sb::NSTAGE * sb::HB * tl.stage_row_bytes + (size_t)sb::NPROD * tl.npb * pbuf;
+    size_t s = (size_t)2 * sb::FPROD * sb::HB * tl.stage_row_bytes + (size_t)sb::FPROD * tl.npb * pbuf;
     // cap residency at 512 / tmem_cols CTAs per SM by asking for enough shared
     // memory, so no CTA ever waits inside tcgen05.alloc
     return std::max(s, residency_floor(512 / tl.tmem_cols));
@@ -223,7 +223,7 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, in
   int smem_per_sm = 233472, regs_per_sm = 65536;
   cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   cudaDeviceGetAttribute(&regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-  const int threads = (m == sb::Mode::Fused) ? sb::FUSED_THREADS : sb::WS;
+  const int threads = (m == sb::Mode::Fused) ? sb::FTHREADS : sb::WS;
   const int regs_per_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (threads / 32);
   occ = std::min(2048 / threads, regs_per_sm / std::max(1, regs_per_cta));
   occ = std::min<long long>(occ, (long long)smem_per_sm / (long long)(smem + fa.sharedSizeBytes + 1024));
@@ -284,7 +284,7 @@ int launch_cols(const void* fn, const Launch& L, const int* mid_in, float* dst, 
 int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, const sb::Geometry& g,
                  const sb::Taps& t, int* status, cudaStream_t stream) {
   void* args[] = {(void*)&src, (void*)&dst, (void*)&g, (void*)&t, (void*)&L.tl, (void*)&status};
-  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::FUSED_THREADS), args, L.smem, stream);
+  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::FTHREADS), args, L.smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   return SB_OK;
 }

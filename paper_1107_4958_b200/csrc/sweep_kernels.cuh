@@ -710,34 +710,39 @@ constexpr int NPROD = 2;
 constexpr int FUSED_THREADS = 32 * (NCONS + NPROD);
 constexpr int NSTAGE = 2 * NPROD;  // staged bands (each producer warp double-buffers its own)
 constexpr int NPBUF = 2 * NPROD;   // prefix buffers (each producer warp owns two)
+// fused kernel: 4 consumer warps + FPROD producer warps (each owns every FPROD-th band)
+constexpr int FCONS = WS / 32;
+constexpr int FPROD = 4;
+constexpr int FTHREADS = 32 * (FCONS + FPROD);
+constexpr int FPBUF = 2 * FPROD;
 
 template <typename Tin, int K>
-__global__ void __launch_bounds__(FUSED_THREADS, 3)
+__global__ void __launch_bounds__(FTHREADS, 2)
     fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
-  __shared__ __align__(8) uint64_t bar_full[NPBUF], bar_empty[NPBUF];
+  __shared__ __align__(8) uint64_t bar_full[FPBUF], bar_empty[FPBUF];
   const int strip = blockIdx.x % tl.nstrips;
   const long long item = blockIdx.x / tl.nstrips;
   const int ch = blockIdx.y;
   const int x0 = strip * WS;
   const int xb = x0 - tl.xoff;
   const int warp = threadIdx.x >> 5;
-  const bool producer = warp >= NCONS;
+  const bool producer = warp >= FCONS;
   const int wh = g.oy1 - g.oy0;  // rows of each image this launch outputs
   const long long total = (long long)g.nimg * wh;
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const bool packed = (sizeof(Tin) == 1) && tl.packed;
   const int pbuf_words = packed ? (HB / 2) * LSP : HB * LS;
-  unsigned char* stage = smem;                                       // 2 producers x 2 staged bands
-  int* Pbase = (int*)(smem + NSTAGE * HB * tl.stage_row_bytes);      // NPBUF prefix buffers
+  unsigned char* stage = smem;                                        // FPROD producers x 2 staged bands
+  int* Pbase = (int*)(smem + 2 * FPROD * HB * tl.stage_row_bytes);    // FPROD x npb prefix buffers
   const int D = tl.D;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NPBUF; ++i) {
+    for (int i = 0; i < FPROD * tl.npb; ++i) {
       mbar_init(&bar_full[i], 32);  // one producer warp fills a prefix buffer
-      mbar_init(&bar_empty[i], 32 * NCONS);
+      mbar_init(&bar_empty[i], 32 * FCONS);
     }
   }
   if (warp == 0) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
@@ -747,10 +752,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
 
   if (producer) {
     // ------------------------------------------------ producer warps
-    // Producer warp pw owns the bands with global index gb = pw (mod 2): it stages
+    // Producer warp pw owns the bands with global index gb = pw (mod FPROD): it stages
     // them into its private pair of buffers (prefetching its next band) and scans
     // them into prefix buffer pw, so the producers never synchronise with each other.
-    const int lane = threadIdx.x & 31, pw = warp - NCONS;
+    const int lane = threadIdx.x & 31, pw = warp - FCONS;
     const bool edge = (xb < 0) || (xb + tl.L > g.W);
     const int st_lo = max(xb, 0) * g.in_px * g.es;
     const int st_hi = min(xb + tl.L, g.W) * g.in_px * g.es;
@@ -768,34 +773,37 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
       const int vstart = a - 1 - t.pmax;
       const int count = (b - a) + 2 * t.pmax + 1;
       const int nbands = (count + HB - 1) / HB;
-      const int first = (int)((pw - gb0) & 1u);  // first band of this segment owned by this warp
+      const int first = (int)(((uint32_t)pw + FPROD * 64u - gb0 % FPROD) % FPROD);  // first owned band
       if (first < nbands)
         issue_stage<Tin>(mystage, src_img, g, tl, xb, vstart + first * HB, min(HB, count - first * HB), st_lo,
                          st_nchunk, st_magic, st_hi16, st_hi, lane, 32);
       int sb = 0;
-      for (int pb = first; pb < nbands; pb += 2, sb ^= 1) {
+      for (int pb = first; pb < nbands; pb += FPROD, sb ^= 1) {
         const uint32_t gb = gb0 + pb;
         const int n = min(HB, count - pb * HB);
         unsigned char* cur = mystage + sb * HB * tl.stage_row_bytes;
         cp_async_wait_all();  // this band landed (the next one is issued below)
         __syncwarp();
-        if (pb + 2 < nbands)
-          issue_stage<Tin>(mystage + (sb ^ 1) * HB * tl.stage_row_bytes, src_img, g, tl, xb, vstart + (pb + 2) * HB,
-                           min(HB, count - (pb + 2) * HB), st_lo, st_nchunk, st_magic, st_hi16, st_hi, lane, 32);
+        if (pb + FPROD < nbands)
+          issue_stage<Tin>(mystage + (sb ^ 1) * HB * tl.stage_row_bytes, src_img, g, tl, xb,
+                           vstart + (pb + FPROD) * HB, min(HB, count - (pb + FPROD) * HB), st_lo, st_nchunk, st_magic,
+                           st_hi16, st_hi, lane, 32);
         if (edge) {
           fixup_edges(cur, g, tl, xb, n, lane, 32);
           __syncwarp();
         }
         // this producer's (gb >> 1)-th band -> its buffer (gb >> 1) % npb, used for the
         // ((gb >> 1) / npb)-th time
-        const uint32_t kb = gb >> 1;
+        const uint32_t kb = gb / FPROD;
         const int pbi = pw * tl.npb + (int)(kb % (uint32_t)tl.npb);
         int* P = Pbase + pbi * pbuf_words;
         mbar_wait(&bar_empty[pbi], ((kb / (uint32_t)tl.npb) & 1) ^ 1);  // consumers done with it
+#ifndef SB_EXP_NOSCAN
         if (packed)
           scan_rows_packed(cur, (uint32_t*)P, tl, 0, 1);
         else
           scan_rows<Tin>(cur, P, g, t, tl, ch, n, status, 0, 1);
+#endif
         mbar_arrive(&bar_full[pbi]);
       }
       gb0 += (uint32_t)nbands;
@@ -819,8 +827,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
       int out_next = a, out_mod = 0, prod_slot = 0;
       for (int pb = 0; pb < nbands; ++pb, ++gb) {
         const int n = min(HB, count - pb * HB);
-        const uint32_t kb = gb >> 1;
-        const int pbi = (int)(gb & 1) * tl.npb + (int)(kb % (uint32_t)tl.npb);
+        const uint32_t kb = gb / FPROD;
+        const int pbi = (int)(gb % FPROD) * tl.npb + (int)(kb % (uint32_t)tl.npb);
         const int* P = Pbase + pbi * pbuf_words;
         float rv[HB];
         mbar_wait(&bar_full[pbi], (kb / (uint32_t)tl.npb) & 1);
@@ -867,7 +875,12 @@ __global__ void __launch_bounds__(FUSED_THREADS, 3)
             trail_s[i] = tr >= D ? tr - D : tr;
           }
           float ov[HB];
+#ifndef SB_EXP_NOCOL
           column_band_tmem<K>(tlane, lead_s, trail_s, box, t, ov);
+#else
+#pragma unroll
+          for (int r = 0; r < HB; ++r) ov[r] = (float)lead_s[r % K];
+#endif
           if (active) {
             float* dptr = dst + (long long)img * g.out_img + (long long)(out_next - g.oy0) * g.out_row +
                           (long long)(x0 + c) * g.out_px + ch;
