@@ -162,6 +162,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Wait with exponential back-off sleep: for warps that usually run ahead (producers),
+// so their polling does not take issue slots from the warps they wait for.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  unsigned ns = 32;
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 1024 ? 2 * ns : ns;
+  }
+}
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -795,9 +813,9 @@ __global__ void __launch_bounds__(FTHREADS, 2)
         // this producer's (gb >> 1)-th band -> its buffer (gb >> 1) % npb, used for the
         // ((gb >> 1) / npb)-th time
         const uint32_t kb = gb / FPROD;
-        const int pbi = pw * tl.npb + (int)(kb % (uint32_t)tl.npb);
+        const int pbi = pw * tl.npb + (int)(kb & (uint32_t)(tl.npb - 1));  // npb is 1 or 2
         int* P = Pbase + pbi * pbuf_words;
-        mbar_wait(&bar_empty[pbi], ((kb / (uint32_t)tl.npb) & 1) ^ 1);  // consumers done with it
+        mbar_wait_sleep(&bar_empty[pbi], ((kb >> (tl.npb - 1)) & 1) ^ 1);  // consumers done with it
 #ifndef SB_EXP_NOSCAN
         if (packed)
           scan_rows_packed(cur, (uint32_t*)P, tl, 0, 1);
@@ -828,10 +846,10 @@ __global__ void __launch_bounds__(FTHREADS, 2)
       for (int pb = 0; pb < nbands; ++pb, ++gb) {
         const int n = min(HB, count - pb * HB);
         const uint32_t kb = gb / FPROD;
-        const int pbi = (int)(gb % FPROD) * tl.npb + (int)(kb % (uint32_t)tl.npb);
+        const int pbi = (int)(gb % FPROD) * tl.npb + (int)(kb & (uint32_t)(tl.npb - 1));
         const int* P = Pbase + pbi * pbuf_words;
         float rv[HB];
-        mbar_wait(&bar_full[pbi], (kb / (uint32_t)tl.npb) & 1);
+        mbar_wait(&bar_full[pbi], (kb >> (tl.npb - 1)) & 1);
         if (packed)
           band_rows_packed<K>((const uint32_t*)P, c, t, tl, rv);
         else
