@@ -439,12 +439,13 @@ __device__ __forceinline__ void band_rows_packed(const uint32_t* __restrict__ P,
   }
 }
 
-// Column pass over one output band from the TMEM ring (slot windows contiguous
-// thanks to the mirrored first band): per box two 16-column loads, then the
-// exact running box sum and the weighted output for 16 rows.
+// Column pass over one output band from the TMEM ring, which holds the running
+// column PREFIX C of the rounded row values (exact int32, wraps): the box sum of
+// slice i at row y is C(y+p_i) - C(y-p_i-1), a difference of two 16-row windows
+// (contiguous thanks to the mirrored first band), with no running state.
 template <int K>
 __device__ __forceinline__ void column_band_tmem(uint32_t tlane, const int (&lead_s)[K], const int (&trail_s)[K],
-                                                 int (&box)[K], const Taps& t, float (&out)[HB]) {
+                                                 const Taps& t, float (&out)[HB]) {
 #pragma unroll
   for (int r = 0; r < HB; ++r) out[r] = 0.0f;
 #pragma unroll
@@ -453,14 +454,9 @@ __device__ __forceinline__ void column_band_tmem(uint32_t tlane, const int (&lea
     tmem_ld16(tlane + (uint32_t)lead_s[i], lv);
     tmem_ld16(tlane + (uint32_t)trail_s[i], tv);
     tmem_wait_ld();
-    int bx = box[i];
     const float w = t.w_col[i];
 #pragma unroll
-    for (int r = 0; r < HB; ++r) {
-      bx += (int)lv[r] - (int)tv[r];
-      out[r] = fmaf(w, (float)bx, out[r]);
-    }
-    box[i] = bx;
+    for (int r = 0; r < HB; ++r) out[r] = fmaf(w, i2f_fast(lv[r] - tv[r]), out[r]);  // exact box sum
   }
 }
 
@@ -839,10 +835,8 @@ __global__ void __launch_bounds__(FTHREADS, 2)
       T = (long long)img * wh + (b - g.oy0);
       const int count = (b - a) + 2 * t.pmax + 1;
       const int nbands = (count + HB - 1) / HB;
-      int box[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) box[i] = 0;
       int out_next = a, out_mod = 0, prod_slot = 0;
+      int cprefix = 0;  // running column prefix of the rounded row values (mid quanta, wraps)
       for (int pb = 0; pb < nbands; ++pb, ++gb) {
         const int n = min(HB, count - pb * HB);
         const uint32_t kb = gb / FPROD;
@@ -856,31 +850,19 @@ __global__ void __launch_bounds__(FTHREADS, 2)
           band_rows<K, LS>(P, c, t.w_row, t, tl, rv);
         mbar_arrive(&bar_empty[pbi]);
         {
-          uint32_t bits[HB];
+          uint32_t cv[HB];
 #pragma unroll
-          for (int r = 0; r < HB; ++r) bits[r] = (uint32_t)__float_as_int(rv[r] + kMagic);  // kMagicBits-biased
-          tmem_st16(tlane + (uint32_t)prod_slot, bits);
-          if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, bits);  // mirror: lag windows never wrap
+          for (int r = 0; r < HB; ++r) {
+            cprefix += __float_as_int(rv[r] + kMagic) - kMagicBits;  // round to the mid quantum
+            cv[r] = (uint32_t)cprefix;
+          }
+          tmem_st16(tlane + (uint32_t)prod_slot, cv);
+          if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, cv);  // mirror: lag windows never wrap
           tmem_wait_st();
         }
         const int produced = pb * HB + n;
         prod_slot += HB;
         prod_slot = prod_slot >= D ? 0 : prod_slot;
-        if (produced >= 2 * t.pmax + 1 && produced - n < 2 * t.pmax + 1) {
-          for (int u0 = 0; u0 <= 2 * t.pmax; u0 += HB) {
-            uint32_t v[HB];
-            tmem_ld16(tlane + (uint32_t)u0, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < HB; ++j) {
-              const int u = u0 + j;
-              const int au = u > t.pmax ? u - t.pmax : t.pmax - u;
-#pragma unroll
-              for (int i = 0; i < K; ++i)
-                if (u <= 2 * t.pmax && au <= t.p[i]) box[i] += (int)v[j] - kMagicBits;
-            }
-          }
-        }
         while (out_next < b) {
           const int nb = min(HB, b - out_next);
           if (produced < (out_next - a) + nb + 2 * t.pmax + 1) break;
@@ -894,7 +876,7 @@ __global__ void __launch_bounds__(FTHREADS, 2)
           }
           float ov[HB];
 #ifndef SB_EXP_NOCOL
-          column_band_tmem<K>(tlane, lead_s, trail_s, box, t, ov);
+          column_band_tmem<K>(tlane, lead_s, trail_s, t, ov);
 #else
 #pragma unroll
           for (int r = 0; r < HB; ++r) ov[r] = (float)lead_s[r % K];
