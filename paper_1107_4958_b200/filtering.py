@@ -161,6 +161,10 @@ def separable_filter_batch(images, kernel: SliceKernel, *, channels_last: bool =
     preallocated contiguous float32 tensor: on the GPU it is written in place,
     on the host (ideally pinned) the result is copied into it.
     """
+    torch_mod = _torch()
+    if (isinstance(images, torch_mod.Tensor) and not images.is_cuda and out is not None and not out.is_cuda
+            and images.dim() >= 3 and (images.dim() == 4 or not channels_last) and images.shape[0] >= 4):
+        return _pipelined_host_batch(images, kernel, channels_last, value_bound, out, check)
     dev = _Device(images)
     x = dev.tensor
     if channels_last:
@@ -206,6 +210,63 @@ def separable_filter_batch(images, kernel: SliceKernel, *, channels_last: bool =
     )
     _raise_for(code)
     return dev.finish(result, status, check, host_out)
+
+
+def _pipelined_host_batch(images, kernel, channels_last, value_bound, out, check, chunks: int = 8):
+    """Host batch -> host result with the PCIe copies overlapped with the kernel.
+
+    The batch is cut into ``chunks`` image groups; group i is copied in on one
+    stream while group i-1 is filtered on another and group i-2 copied out on a
+    third (three device buffers rotate).  Every group is an independent
+    ``separable_filter_batch`` call, so the result is identical to the
+    one-shot call (float input without ``value_bound`` gets its bound per group).
+    """
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("sliceblur_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    if out.dtype != torch.float32 or not out.is_contiguous() or out.numel() != images.numel():
+        raise ValueError("out must be a contiguous float32 tensor of the input's size")
+    b = images.shape[0]
+    chunks = max(1, min(chunks, b))
+    bounds = [b * i // chunks for i in range(chunks + 1)]
+    per = max(bounds[i + 1] - bounds[i] for i in range(chunks))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    nbuf = 3
+    xin = [torch.empty((per,) + tuple(images.shape[1:]), dtype=images.dtype, device=dev) for _ in range(nbuf)]
+    yout = [torch.empty((per,) + tuple(images.shape[1:]), dtype=torch.float32, device=dev) for _ in range(nbuf)]
+    s_in, s_run, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    for st in (s_in, s_run, s_out):
+        st.wait_stream(main)
+    done_run = [None] * nbuf
+    done_out = [None] * nbuf
+    for i in range(chunks):
+        lo, hi = bounds[i], bounds[i + 1]
+        n = hi - lo
+        k = i % nbuf
+        with torch.cuda.stream(s_in):
+            if done_run[k] is not None:
+                s_in.wait_event(done_run[k])  # input buffer k no longer read
+            xin[k][:n].copy_(images[lo:hi], non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(s_in)
+        with torch.cuda.stream(s_run):
+            s_run.wait_event(ev_in)
+            if done_out[k] is not None:
+                s_run.wait_event(done_out[k])  # output buffer k copied out
+            separable_filter_batch(xin[k][:n], kernel, channels_last=channels_last, value_bound=value_bound,
+                                   out=yout[k][:n], check=check)
+            done_run[k] = torch.cuda.Event()
+            done_run[k].record(s_run)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(done_run[k])
+            out[lo:hi].copy_(yout[k][:n], non_blocking=True)
+            done_out[k] = torch.cuda.Event()
+            done_out[k].record(s_out)
+    for st in (s_in, s_run, s_out):
+        main.wait_stream(st)
+    s_out.synchronize()
+    return out
 
 
 def separable_filter_window(image, kernel: SliceKernel, row_begin: int, row_end: int, *, channels_last: bool = False,

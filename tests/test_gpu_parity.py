@@ -238,3 +238,14 @@ def test_row_window_strips_match_full_image(k, sigma):
         np.testing.assert_array_equal(np.concatenate(parts), full)
     ref = O.separable_filter_2d(img, kern.radii, kern.weights, threads=THREADS)
     assert np.abs(full - ref).max() <= BAR
+
+
+def test_pipelined_host_batch_matches_device_call():
+    # host (pinned) tensors in and out: the chunked copy/compute pipeline must give the
+    # same result as the one-shot device call
+    imgs = torch.from_numpy(synth.u8_batch(12, 256, 320, seed0=77)).pin_memory()
+    kern = A.table_kernel(3, 10.0)
+    out_host = torch.empty(imgs.shape, dtype=torch.float32).pin_memory()
+    F.separable_filter_batch(imgs, kern, out=out_host)
+    ref = F.separable_filter_batch(imgs.cuda(), kern).cpu()
+    assert torch.equal(out_host, ref)
