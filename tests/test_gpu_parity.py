@@ -249,3 +249,55 @@ def test_pipelined_host_batch_matches_device_call():
     F.separable_filter_batch(imgs, kern, out=out_host)
     ref = F.separable_filter_batch(imgs.cuda(), kern).cpu()
     assert torch.equal(out_host, ref)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_shapes_dtypes_kernels(seed):
+    # randomized sweep: odd shapes (strips not multiples of 128, fewer rows than a band),
+    # every source dtype, interleaved channels, batches, k = 1..8 slices with p = 0 and
+    # negative weights, radii small (fused sweep) and large (two-launch path)
+    rng = np.random.default_rng(9000 + seed)
+    h, w = int(rng.integers(1, 400)), int(rng.integers(1, 400))
+    dtype = [np.uint8, np.uint16, np.float32, np.float64][seed % 4]
+    ch = int(rng.integers(1, 4)) if seed % 3 == 0 else 1
+    batch = int(rng.integers(1, 4))
+    k = int(rng.integers(1, 9))
+    reach = min(h, w) - 1
+    if reach + 1 < k:
+        k = reach + 1
+    big = seed % 5 == 0 and reach > 120
+    lo = 90 if big else 0
+    pool = np.arange(lo, reach + 1) if big else np.arange(0, min(reach, 60) + 1)
+    if pool.size < k:
+        pool = np.arange(0, reach + 1)
+    radii = np.sort(rng.choice(pool, size=k, replace=False))
+    weights = rng.uniform(0.1, 1.0, size=k)
+    if k > 1 and seed % 2:
+        weights[int(rng.integers(k))] *= -0.3
+    kern = A.SliceKernel(radii, weights).normalized()
+    scale = {np.uint8: 255, np.uint16: 65535, np.float32: 255.0, np.float64: 1000.0}[dtype]
+    shape = (batch, h, w, ch) if ch > 1 else (batch, h, w)
+    x = (rng.random(shape) * scale).astype(dtype)
+    got = F.separable_filter_batch(x, kern, channels_last=ch > 1)
+    gabs = float(np.sum(np.abs(kern.weights) * (2 * kern.radii + 1)))
+    tol = BAR * float(scale) / 255.0 * max(1.0, gabs)
+    for bi in range(batch):
+        for c in range(ch):
+            img = x[bi, :, :, c] if ch > 1 else x[bi]
+            ref = O.separable_filter_2d(np.ascontiguousarray(img), kern.radii, kern.weights)
+            res = got[bi, :, :, c] if ch > 1 else got[bi]
+            assert np.abs(res - ref).max() <= tol, (seed, h, w, dtype, ch, batch, kern)
+
+
+def test_kernel_too_large_and_1d_edges():
+    kern = A.SliceKernel((0, 3), (0.5, 0.5 / 7)).normalized()
+    with pytest.raises(F.KernelTooLargeError):
+        F.separable_filter_2d(np.zeros((3, 50), np.float32), kern)
+    # 1D signal exactly one sample longer than the largest radius (both clamps apply)
+    sig = np.random.default_rng(1).random(4) * 255
+    got = F.slice_filter_1d(sig, kern)
+    ref = O.filter_rows(sig[None, :], kern.radii, kern.weights)[0]
+    assert np.abs(got - ref).max() <= BAR
+    # single-pixel image with a p = 0 kernel is the identity
+    one = np.array([[42.0]], np.float32)
+    assert F.separable_filter_2d(one, A.SliceKernel((0,), (1.0,)))[0, 0] == pytest.approx(42.0, abs=BAR)
