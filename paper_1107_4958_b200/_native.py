@@ -11,7 +11,7 @@ import ctypes
 import os
 
 LIB_NAME = "libsliceblur_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("SB_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 SB_OK = 0
 SB_ERR_INVALID_ARGUMENT = 1

@@ -146,8 +146,13 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
   tl.lanes_per_row = lpr;
   tl.stage_row_bytes = ceil16(tl.L * staged_ch * es);
   tl.ls = (m == sb::Mode::Fused) ? sb::LS : tl.L;
-  tl.packed = (m == sb::Mode::Fused && u8_single && nchunk <= 32 && tl.L <= sb::LSP) ? 1 : 0;  // exact 16-bit prefixes
-  tl.npb = tl.packed ? 2 : 1;  // unpacked prefix buffers are large: one per producer
+  tl.packed = (m == sb::Mode::Fused && u8_single && ((tl.L + 63) & ~63) <= sb::LSP) ? 1 : 0;  // float2 prefixes
+  if (tl.packed) {
+    // the scan covers whole 64-column quarters; rows an odd multiple of 16 bytes apart
+    tl.L = (tl.L + 63) & ~63;
+    tl.stage_row_bytes = tl.L + 16;
+  }
+  tl.npb = 1;  // one prefix buffer per producer warp (each owns every FPROD-th band)
   tl.D = ((2 * pmax + 2 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;  // multiple of HB
   if (m == sb::Mode::ColsFromMid) {
     // The ring must hold every LEAD window: lag <= pmax - pmin + 3*HB behind the newest row.
@@ -173,7 +178,7 @@ size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
   if (m == sb::Mode::ColsFromMid) return residency_floor(512 / tl.tmem_cols);
   if (m == sb::Mode::Fused) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
-    const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP * sizeof(int) : (size_t)sb::HB * sb::LS * sizeof(int);
+    const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP2 * sizeof(float2) : (size_t)sb::HB * sb::LS * sizeof(int);
     size_t s = (size_t)2 * sb::FPROD * sb::HB * tl.stage_row_bytes + (size_t)sb::FPROD * tl.npb * pbuf;
     // cap residency at 512 / tmem_cols CTAs per SM by asking for enough shared
     // memory, so no CTA ever waits inside tcgen05.alloc

@@ -47,6 +47,7 @@ constexpr int NWARPS = WS / 32;
 constexpr int CH = 16;          // px per scan chunk (one lane)
 constexpr int LS = 512;         // prefix row stride in words (compile-time: immediate offsets)
 constexpr int LSP = 256;        // packed-prefix row stride in words (uint8, pmax <= 63)
+constexpr int LSP2 = LSP + 2;   // float2-prefix row stride: 2064 B = 16 (mod 128), conflict-free stores
 constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + kMagic rounds x to an integer (|x| < 2^22)
 constexpr int kMagicBits = 0x4B400000;  // bits(kMagic + n) = kMagicBits + n
 
@@ -397,6 +398,69 @@ __device__ __forceinline__ void scan_rows_packed(const unsigned char* buf, uint3
   }
 }
 
+// uint8, one channel, float prefixes: rows q and q+8 of the band share float2 q of
+// P (x = row q, y = row q+8), stored as the fp32 numbers 2^23 + prefix.  For
+// 0 <= v < 2^23 the bit pattern of 2^23 + v is 0x4B000000 + v, so the scan is
+// integer: one IDP4A per pixel turns a word of four bytes into a prefix
+// (dp4a(word, 0x00010101, base) = base + b0 + b1 + b2), and a box sum is one
+// exact fp32 subtraction (FADD2 on a row pair) of two such values.
+// Lane = seg * 8 + q scans columns [seg*4*NW, (seg+1)*4*NW) of rows q and q+8;
+// the four segment offsets come from a two-step shuffle scan of packed 16-bit
+// totals (<= 256*255 < 2^16).  Staging rows are an odd multiple of 16 bytes
+// apart and P rows 2064 bytes, so each 8-lane phase of the 128-bit loads and
+// stores touches 8 distinct bank groups.
+template <int NW>
+__device__ __forceinline__ void scan_rows_b2(const unsigned char* buf, float2* __restrict__ P, int srb) {
+  const int lane = threadIdx.x & 31;
+  const int q = lane & 7, seg = lane >> 3;
+  const unsigned char* ra = buf + q * srb + seg * (4 * NW);
+  const unsigned char* rb = ra + (HB / 2) * srb;
+  uint32_t wa[NW], wb[NW];
+#pragma unroll
+  for (int j = 0; j < NW / 4; ++j) {
+    const uint4 x = *(const uint4*)(ra + 16 * j);
+    const uint4 y = *(const uint4*)(rb + 16 * j);
+    wa[4 * j] = x.x, wa[4 * j + 1] = x.y, wa[4 * j + 2] = x.z, wa[4 * j + 3] = x.w;
+    wb[4 * j] = y.x, wb[4 * j + 1] = y.y, wb[4 * j + 2] = y.z, wb[4 * j + 3] = y.w;
+  }
+  uint32_t ta = 0, tb = 0;
+#pragma unroll
+  for (int j = 0; j < NW; ++j) {
+    ta = __dp4a(wa[j], 0x01010101u, ta);
+    tb = __dp4a(wb[j], 0x01010101u, tb);
+  }
+  const uint32_t t = ta | (tb << 16);
+  uint32_t inc = t;
+  uint32_t y = __shfl_up_sync(0xffffffffu, inc, 8);
+  if (seg >= 1) inc += y;
+  y = __shfl_up_sync(0xffffffffu, inc, 16);
+  if (seg >= 2) inc += y;
+  const uint32_t ex = inc - t;
+  uint32_t ba = 0x4B000000u + (ex & 0xFFFFu), bb = 0x4B000000u + (ex >> 16);
+  float2* dst = P + q * LSP2 + seg * (4 * NW);
+#pragma unroll
+  for (int j = 0; j < NW; ++j) {
+    const uint32_t a0 = __dp4a(wa[j], 0x00000001u, ba), b0 = __dp4a(wb[j], 0x00000001u, bb);
+    const uint32_t a1 = __dp4a(wa[j], 0x00000101u, ba), b1 = __dp4a(wb[j], 0x00000101u, bb);
+    const uint32_t a2 = __dp4a(wa[j], 0x00010101u, ba), b2 = __dp4a(wb[j], 0x00010101u, bb);
+    ba = __dp4a(wa[j], 0x01010101u, ba);
+    bb = __dp4a(wb[j], 0x01010101u, bb);
+    float4* d4 = (float4*)(dst + 4 * j);
+    d4[0] = make_float4(__uint_as_float(a0), __uint_as_float(b0), __uint_as_float(a1), __uint_as_float(b1));
+    d4[1] = make_float4(__uint_as_float(a2), __uint_as_float(b2), __uint_as_float(ba), __uint_as_float(bb));
+  }
+}
+
+__device__ __forceinline__ void scan_rows_b2_dispatch(const unsigned char* buf, float2* __restrict__ P,
+                                                      const Tiling& tl) {
+  switch (tl.L >> 6) {  // packed tilings have L a multiple of 64, at most 256
+    case 1: scan_rows_b2<4>(buf, P, tl.stage_row_bytes); break;
+    case 2: scan_rows_b2<8>(buf, P, tl.stage_row_bytes); break;
+    case 3: scan_rows_b2<12>(buf, P, tl.stage_row_bytes); break;
+    default: scan_rows_b2<16>(buf, P, tl.stage_row_bytes); break;
+  }
+}
+
 // ---------------------------------------------------------------- pass 1: row values
 // Row-filtered values of the HB staged rows at strip column c, accumulated box by
 // box so every shared-memory load is (lag pointer) + (row * L): the lag pointers
@@ -435,6 +499,26 @@ __device__ __forceinline__ void band_rows_packed(const uint32_t* __restrict__ P,
       const uint32_t d = pl[q * LSP] - pt[q * LSP];  // two exact 16-bit box sums
       acc[q] = fmaf(wl, i2f_fast(d & 0xFFFFu), acc[q]);
       acc[q + HB / 2] = fmaf(wl, i2f_fast(d >> 16), acc[q + HB / 2]);
+    }
+  }
+}
+
+// Float-prefix uint8 variant: float2 q holds rows q (x) and q+8 (y); the box sum is
+// an exact packed subtraction and the weighted sum one packed FFMA2 per box.
+template <int K>
+__device__ __forceinline__ void band_rows_f2(const float2* __restrict__ P, int c, const Taps& t, const Tiling& tl,
+                                             float2 (&acc)[HB / 2]) {
+  const int base = c + tl.xoff;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const float2* pl = P + base + t.p[i];
+    const float2* pt = P + base - t.p[i] - 1;
+    const float2 w2 = make_float2(t.w_row[i], t.w_row[i]);
+#pragma unroll
+    for (int q = 0; q < HB / 2; ++q) {
+      const float2 l = pl[q * LSP2], r = pt[q * LSP2];
+      const float2 d = __fadd2_rn(l, make_float2(-r.x, -r.y));  // exact box sums of rows q, q+8
+      acc[q] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, acc[q]);
     }
   }
 }
@@ -748,7 +832,7 @@ __global__ void __launch_bounds__(FTHREADS, 2)
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const bool packed = (sizeof(Tin) == 1) && tl.packed;
-  const int pbuf_words = packed ? (HB / 2) * LSP : HB * LS;
+  const int pbuf_words = packed ? HB * LSP2 : HB * LS;  // packed: HB/2 float2 rows
   unsigned char* stage = smem;                                        // FPROD producers x 2 staged bands
   int* Pbase = (int*)(smem + 2 * FPROD * HB * tl.stage_row_bytes);    // FPROD x npb prefix buffers
   const int D = tl.D;
@@ -814,7 +898,7 @@ __global__ void __launch_bounds__(FTHREADS, 2)
         mbar_wait_sleep(&bar_empty[pbi], ((kb >> (tl.npb - 1)) & 1) ^ 1);  // consumers done with it
 #ifndef SB_EXP_NOSCAN
         if (packed)
-          scan_rows_packed(cur, (uint32_t*)P, tl, 0, 1);
+          scan_rows_b2_dispatch(cur, (float2*)P, tl);
         else
           scan_rows<Tin>(cur, P, g, t, tl, ch, n, status, 0, 1);
 #endif
@@ -844,16 +928,26 @@ __global__ void __launch_bounds__(FTHREADS, 2)
         const int* P = Pbase + pbi * pbuf_words;
         float rv[HB];
         mbar_wait(&bar_full[pbi], (kb >> (tl.npb - 1)) & 1);
-        if (packed)
-          band_rows_packed<K>((const uint32_t*)P, c, t, tl, rv);
-        else
+        if (packed) {
+          float2 r2[HB / 2];
+          band_rows_f2<K>((const float2*)P, c, t, tl, r2);
+#pragma unroll
+          for (int q = 0; q < HB / 2; ++q) {
+            r2[q] = __fadd2_rn(r2[q], make_float2(kMagic, kMagic));  // round to the mid quantum
+            rv[q] = r2[q].x;
+            rv[q + HB / 2] = r2[q].y;
+          }
+        } else {
           band_rows<K, LS>(P, c, t.w_row, t, tl, rv);
+#pragma unroll
+          for (int r = 0; r < HB; ++r) rv[r] += kMagic;  // round to the mid quantum
+        }
         mbar_arrive(&bar_empty[pbi]);
         {
           uint32_t cv[HB];
 #pragma unroll
           for (int r = 0; r < HB; ++r) {
-            cprefix += __float_as_int(rv[r] + kMagic) - kMagicBits;  // round to the mid quantum
+            cprefix += __float_as_int(rv[r]) - kMagicBits;
             cv[r] = (uint32_t)cprefix;
           }
           tmem_st16(tlane + (uint32_t)prod_slot, cv);

@@ -18,7 +18,7 @@ if timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/${R}_
 fi
 for c in c3 c5 c4; do
   if timeout 120 python tools/prof_run.py --config $c --iters 3 > $O/${R}_prof_plain_$c.log 2>&1; then
-    timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fused|cols|stream_rows" -s 2 -c 1 \
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fused|cols|stream_rows" -s 2 -c 2 \
       -o $O/${R}_prof_$c -f python tools/prof_run.py --config $c --iters 3 > $O/${R}_ncu_full_$c.log 2>&1
   fi
 done
