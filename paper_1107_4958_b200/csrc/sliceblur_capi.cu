@@ -4,6 +4,8 @@
 // (filtering.py:39-45, 67-73, 76-104): argument checks, the fixed-point quanta
 // (DESIGN.md "Arithmetic"), the choice between the fused single-launch sweep
 // and the two-launch path, and the work decomposition over 148 SMs.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -153,6 +155,11 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
     tl.stage_row_bytes = tl.L + 16;
   }
   tl.npb = 1;  // one prefix buffer per producer warp (each owns every FPROD-th band)
+  if (m == sb::Mode::Fused) {
+    const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP2 * sizeof(float2) : (size_t)sb::HB * sb::LS * sizeof(int);
+    const size_t end = (size_t)2 * sb::FPROD * sb::HB * tl.stage_row_bytes + (size_t)sb::FPROD * tl.npb * pbuf;
+    tl.obuf_off = (int)((end + 127) & ~(size_t)127);
+  }
   tl.D = ((2 * pmax + 2 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;  // multiple of HB
   if (m == sb::Mode::ColsFromMid) {
     // The ring must hold every LEAD window: lag <= pmax - pmin + 3*HB behind the newest row.
@@ -178,8 +185,8 @@ size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
   if (m == sb::Mode::ColsFromMid) return residency_floor(512 / tl.tmem_cols);
   if (m == sb::Mode::Fused) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
-    const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP2 * sizeof(float2) : (size_t)sb::HB * sb::LS * sizeof(int);
-    size_t s = (size_t)2 * sb::FPROD * sb::HB * tl.stage_row_bytes + (size_t)sb::FPROD * tl.npb * pbuf;
+    // + FCONS x 2 output bands of HB x 32 floats staged for TMA tensor stores
+    size_t s = (size_t)tl.obuf_off + 128 + (size_t)sb::FCONS * 2 * sb::HB * 32 * sizeof(float);
     // cap residency at 512 / tmem_cols CTAs per SM by asking for enough shared
     // memory, so no CTA ever waits inside tcgen05.alloc
     return std::max(s, residency_floor(512 / tl.tmem_cols));
@@ -286,9 +293,48 @@ int launch_cols(const void* fn, const Launch& L, const int* mid_in, float* dst, 
   return SB_OK;
 }
 
-int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, const sb::Geometry& g,
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda at link time)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// Output tensor map [image][row][column] (fp32) with a 16 x 32 box: one box per
+// consumer warp and output band.  Clears g.out_bulk when no map can be made.
+void make_output_map(float* dst, sb::Geometry& g, CUtensorMap* map) {
+  std::memset(map, 0, sizeof(*map));
+  if (!g.out_bulk) return;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  const long long rows = g.oy1 - g.oy0;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)rows, (cuuint64_t)g.nimg};
+  const cuuint64_t rstride = (cuuint64_t)g.out_row * 4;
+  const cuuint64_t istride = g.nimg > 1 ? (cuuint64_t)g.out_img * 4 : rstride * (cuuint64_t)rows;
+  const cuuint64_t strides[2] = {rstride, istride};
+  const cuuint32_t box[3] = {32, (cuuint32_t)sb::HB, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (!enc || enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)dst, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    g.out_bulk = 0;
+}
+
+int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, const sb::Geometry& g0,
                  const sb::Taps& t, int* status, cudaStream_t stream) {
-  void* args[] = {(void*)&src, (void*)&dst, (void*)&g, (void*)&t, (void*)&L.tl, (void*)&status};
+  sb::Geometry g = g0;
+  alignas(64) CUtensorMap omap;
+  make_output_map(dst, g, &omap);
+  void* args[] = {(void*)&src, (void*)&dst, (void*)&g, (void*)&t, (void*)&L.tl, (void*)&status, (void*)&omap};
   cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::FTHREADS), args, L.smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   return SB_OK;
@@ -365,6 +411,8 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
   g.oy1 = (int)row_end;
   g.aligned16 = ((uintptr_t)src % 16 == 0) && ((src_row_stride * g.es) % 16 == 0) &&
                 (batch == 1 || (src_image_stride * g.es) % 16 == 0);
+  g.out_bulk = channels == 1 && ((uintptr_t)dst % 16 == 0) && ((dst_row_stride * 4) % 16 == 0) &&
+               (batch == 1 || (dst_image_stride * 4) % 16 == 0) && getenv("SB_NO_TMA_STORE") == nullptr;
   const long long total_rows = (long long)batch * (row_end - row_begin);  // rows the column sweep outputs
   const long long all_rows = (long long)batch * height;                   // rows the row pass produces
   const bool u8_single = (src_dtype == SB_DTYPE_U8 && channels == 1);

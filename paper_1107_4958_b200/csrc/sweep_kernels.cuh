@@ -35,6 +35,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "sliceblur_b200.h"
@@ -62,6 +63,7 @@ struct Geometry {
   int H, W, nimg;
   int oy0, oy1;                // output row window of every image (column sweeps write rows oy0..oy1-1)
   int aligned16;               // rows are 16-byte aligned: cp.async 16 B staging
+  int out_bulk;                // one channel, 16-byte aligned rows: full output bands leave by TMA tensor stores
 };
 
 struct Taps {
@@ -87,6 +89,7 @@ struct Tiling {
   int tmem_cols;        // tensor-memory columns allocated for the ring (power of two, >= D + HB)
   int sw;               // strip width in columns (WS for sweeps, wider for the row pass alone)
   int npb;              // fused: prefix buffers per producer warp (1 or 2)
+  int obuf_off;         // fused: byte offset of the output staging bands in shared memory
 };
 
 enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3 };
@@ -115,6 +118,18 @@ __device__ __forceinline__ int ld_keep(const int* p, uint64_t pol) {
 }
 __device__ __forceinline__ void st_stream(float* p, float v) {
   asm volatile("st.global.cs.f32 [%0], %1;\n" ::"l"(p), "f"(v));
+}
+// ---- TMA tensor stores from shared memory (async proxy)
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* ssrc, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"(smem_u32(ssrc)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
 // ---- tensor memory (tcgen05): the fused column ring.  Thread c of the CTA owns
@@ -530,17 +545,25 @@ __device__ __forceinline__ void band_rows_f2(const float2* __restrict__ P, int c
 template <int K>
 __device__ __forceinline__ void column_band_tmem(uint32_t tlane, const int (&lead_s)[K], const int (&trail_s)[K],
                                                  const Taps& t, float (&out)[HB]) {
-#pragma unroll
-  for (int r = 0; r < HB; ++r) out[r] = 0.0f;
+  float2 o2[HB / 2];
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     uint32_t lv[HB], tv[HB];
     tmem_ld16(tlane + (uint32_t)lead_s[i], lv);
     tmem_ld16(tlane + (uint32_t)trail_s[i], tv);
     tmem_wait_ld();
-    const float w = t.w_col[i];
+    const float2 w2 = make_float2(t.w_col[i], t.w_col[i]);
 #pragma unroll
-    for (int r = 0; r < HB; ++r) out[r] = fmaf(w, i2f_fast(lv[r] - tv[r]), out[r]);  // exact box sum
+    for (int r = 0; r < HB / 2; ++r) {
+      // exact box sums of rows 2r, 2r+1, weighted with one packed FFMA2
+      const float2 d = make_float2(i2f_fast(lv[2 * r] - tv[2 * r]), i2f_fast(lv[2 * r + 1] - tv[2 * r + 1]));
+      o2[r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, o2[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < HB / 2; ++r) {
+    out[2 * r] = o2[r].x;
+    out[2 * r + 1] = o2[r].y;
   }
 }
 
@@ -816,8 +839,9 @@ constexpr int FPBUF = 2 * FPROD;
 
 template <typename Tin, int K>
 __global__ void __launch_bounds__(FTHREADS, 2)
-    fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status) {
-  extern __shared__ __align__(16) unsigned char smem[];
+    fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status,
+                 const __grid_constant__ CUtensorMap omap) {
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
   __shared__ __align__(8) uint64_t bar_full[FPBUF], bar_empty[FPBUF];
   const int strip = blockIdx.x % tl.nstrips;
@@ -835,6 +859,8 @@ __global__ void __launch_bounds__(FTHREADS, 2)
   const int pbuf_words = packed ? HB * LSP2 : HB * LS;  // packed: HB/2 float2 rows
   unsigned char* stage = smem;                                        // FPROD producers x 2 staged bands
   int* Pbase = (int*)(smem + 2 * FPROD * HB * tl.stage_row_bytes);    // FPROD x npb prefix buffers
+  // FCONS x 2 output bands (TMA stores; 128-byte aligned shared addresses)
+  float* obuf = (float*)(smem + (((smem_u32(smem) + tl.obuf_off + 127u) & ~127u) - smem_u32(smem)));
   const int D = tl.D;
 
   if (threadIdx.x == 0) {
@@ -912,6 +938,7 @@ __global__ void __launch_bounds__(FTHREADS, 2)
     const bool active = (x0 + c) < g.W;
     const uint32_t tlane = tmem_base_s + ((uint32_t)(threadIdx.x & ~31) << 16);
     uint32_t gb = 0;
+    int obsel = 0;
     for (long long T = T0; T < T1;) {
       const int img = (int)(T / wh);
       const int a = g.oy0 + (int)(T - (long long)img * wh);
@@ -975,7 +1002,23 @@ __global__ void __launch_bounds__(FTHREADS, 2)
 #pragma unroll
           for (int r = 0; r < HB; ++r) ov[r] = (float)lead_s[r % K];
 #endif
-          if (active) {
+          if (g.out_bulk && nb == HB) {
+            // stage the band (row r of this warp's 32 columns at ob[r][lane]) and let one
+            // TMA tensor store write the 16 x 32 box: no per-row address arithmetic
+            const int lane = threadIdx.x & 31;
+            float* ob = obuf + (warp * 2 + obsel) * (HB * 32);
+            if (lane == 0) bulk_wait_read<1>();  // the store out of this buffer (two bands ago) has read it
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < HB; ++r) ob[r * 32 + lane] = ov[r];
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&omap, ob, x0 + (warp << 5), out_next - g.oy0, img);
+              bulk_commit();
+            }
+            obsel ^= 1;
+          } else if (active) {
             float* dptr = dst + (long long)img * g.out_img + (long long)(out_next - g.oy0) * g.out_row +
                           (long long)(x0 + c) * g.out_px + ch;
             const long long step = g.out_row;
@@ -999,6 +1042,7 @@ __global__ void __launch_bounds__(FTHREADS, 2)
         }
       }
     }
+    if ((threadIdx.x & 31) == 0) bulk_wait_read<0>();  // shared memory must outlive the stores out of it
   }
   tmem_fence_before();
   __syncthreads();

@@ -1,9 +1,15 @@
 #!/bin/bash
-# A/B timing of variant libraries: bash exp/ab.sh cfg lib1 lib2 ...  ("default" = in-tree build)
+# A/B timing of variant libraries: bash tools/ab.sh cfg lib1 lib2 ...
+#   "default" = in-tree build; "env:NAME=VALUE" = in-tree build with that variable set
 cfg=$1; shift
 for rep in 1 2; do
 for lib in "$@"; do
-  if [ "$lib" = default ]; then unset SB_LIB_PATH; else export SB_LIB_PATH=$PWD/$lib; fi
+  unset SB_LIB_PATH SB_NO_TMA_STORE
+  case "$lib" in
+    default) ;;
+    env:*) export "${lib#env:}" ;;
+    *) export SB_LIB_PATH=$PWD/$lib ;;
+  esac
   v=$(timeout 200 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print(d['ms_per_step'], d['value'], d.get('parity',{}).get('max_abs'))")
   echo "$cfg $lib rep$rep: $v"
 done; done
