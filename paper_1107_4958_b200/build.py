@@ -37,8 +37,17 @@ def deps():
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + sorted(glob.glob(os.path.join(INCLUDE, "*.h")))
 
 
+STAMP = OUT + ".flags"
+
+
 def up_to_date() -> bool:
     if not os.path.exists(OUT):
+        return False
+    try:
+        with open(STAMP) as f:
+            if f.read() != os.environ.get("SB_NVCC_EXTRA", ""):
+                return False  # built with other extra flags
+    except OSError:
         return False
     built = os.path.getmtime(OUT)
     return all(os.path.getmtime(p) <= built for p in deps())
@@ -75,6 +84,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = OUT + ".tmp"
     subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs], check=True)
     os.replace(tmp, OUT)
+    with open(STAMP, "w") as f:
+        f.write(os.environ.get("SB_NVCC_EXTRA", ""))
     return OUT
 
 

@@ -841,7 +841,7 @@ template <typename Tin, int K>
 __global__ void __launch_bounds__(FTHREADS, 2)
     fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status,
                  const __grid_constant__ CUtensorMap omap) {
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
   __shared__ __align__(8) uint64_t bar_full[FPBUF], bar_empty[FPBUF];
   const int strip = blockIdx.x % tl.nstrips;
