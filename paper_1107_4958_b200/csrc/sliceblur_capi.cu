@@ -162,14 +162,11 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
   }
   tl.D = ((2 * pmax + 2 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;  // multiple of HB
   if (m == sb::Mode::ColsFromMid) {
-    // The ring must hold every LEAD window: lag <= pmax - pmin + 3*HB behind the newest row.
-    // Trails deeper than the ring are re-read from the plane (kept in L2 by evict_last).
-    // Prefer a 256-column allocation (two CTAs per SM) when the leads fit in it.
-    const int d_full = tl.D;
-    const int d_lead = ((pmax - pmin + 3 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;
-    if (d_full + sb::HB <= 256) tl.D = d_full;
-    else if (d_lead + sb::HB <= 256) tl.D = 256 - sb::HB;
-    else tl.D = std::min(d_full, 512 - sb::HB);
+    // The ring holds every window when it fits tensor memory; otherwise trails deeper than
+    // the ring are re-read from the plane (prefetched through shared memory).  Measured:
+    // a full ring at one CTA per SM beats a 256-column ring with deep re-reads (C4).
+    (void)pmin;
+    tl.D = std::min(tl.D, 512 - sb::HB);
   }
   int cols = 32;
   while (cols < tl.D + sb::HB) cols <<= 1;
@@ -182,7 +179,8 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
 size_t residency_floor(int ctas) { return 233472 / (size_t)(ctas + 1) - 1024 + 16; }
 
 size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
-  if (m == sb::Mode::ColsFromMid) return residency_floor(512 / tl.tmem_cols);
+  if (m == sb::Mode::ColsFromMid)
+    return std::max((size_t)(1 + tl.ndeep) * tl.pf * sb::HB * sb::WS * sizeof(int), residency_floor(512 / tl.tmem_cols));
   if (m == sb::Mode::Fused) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
     // + FCONS x 2 output bands of HB x 32 floats staged for TMA tensor stores
@@ -464,8 +462,23 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
   }
   const void* f2 = pick_kernel(sb::Mode::ColsFromMid, src_dtype, k);
   Launch L2;
-  rc = plan_launch(f2, sb::Mode::ColsFromMid, make_tiling(sb::Mode::ColsFromMid, plan.pmax, channels, 4, false, (int)radii[0]),
-                   plan.pmax, g.W, total_rows, channels, &L2);
+  sb::Tiling ct = make_tiling(sb::Mode::ColsFromMid, plan.pmax, channels, 4, false, (int)radii[0]);
+  // deep trails (older than the ring) of the largest boxes come through shared memory
+  ct.ndeep = 0;
+  for (int d = 0; d < sb::SB_NDEEP && d < k; ++d)
+    if (2 * sb::HB + plan.pmax + (int)radii[k - 1 - d] > ct.D) ct.ndeep = d + 1;
+  {
+    const size_t band = (size_t)sb::HB * sb::WS * sizeof(int);
+    const size_t budget = (512 / ct.tmem_cols) > 1 ? 100 * 1024 : 200 * 1024;
+    const int choices[] = {8, 6, 4, 3, 2};
+    ct.pf = 2;
+    for (int pf : choices)
+      if ((size_t)(1 + ct.ndeep) * pf * band <= budget) {
+        ct.pf = pf;
+        break;
+      }
+  }
+  rc = plan_launch(f2, sb::Mode::ColsFromMid, ct, plan.pmax, g.W, total_rows, channels, &L2);
   if (rc) return rc;
   return launch_cols(f2, L2, mid, dst, g, plan.taps, st);
 }

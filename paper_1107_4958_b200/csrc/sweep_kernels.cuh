@@ -90,6 +90,8 @@ struct Tiling {
   int sw;               // strip width in columns (WS for sweeps, wider for the row pass alone)
   int npb;              // fused: prefix buffers per producer warp (1 or 2)
   int obuf_off;         // fused: byte offset of the output staging bands in shared memory
+  int pf;               // cols: plane bands prefetched ahead (2, 3, 4, 6 or 8)
+  int ndeep;            // cols: largest boxes whose trails are re-read from the plane (0..SB_NDEEP)
 };
 
 enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3 };
@@ -674,16 +676,34 @@ __global__ void __launch_bounds__(WS) rows_kernel(const Tin* __restrict__ src, i
 
 // ---------------------------------------------------------------- column pass from the int32 plane
 // ColsFromMid (large radii): thread c <-> strip column c <-> TMEM lane c.  Each
-// band of HB rows of the R plane is read once (coalesced, one band ahead into
-// registers) and appended to a TMEM ring of D rows (mirrored first band); the
-// k running box sums read their lead/trail windows from the ring, except
-// trails older than the ring (lag > D - HB) which are re-read from the plane
-// (L2-resident: the plane rows a CTA touched 2*pmax rows ago).
+// band of HB rows of the R plane is read once and appended to a TMEM ring of D
+// rows (mirrored first band); the k running box sums read their lead/trail
+// windows from the ring, except trails older than the ring (lag > D - HB),
+// which are re-read from the plane.  All plane
+// reads are cp.async copies of the thread's own column into shared-memory rings
+// issued tl.pf bands ahead (one commit group per band), so HBM latency is hidden
+// without registers and without CTA-wide barriers.
+constexpr int SB_NDEEP = 4;  // deep-trail boxes prefetched through shared memory (the largest ones)
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(sdst)), "l"(gsrc));
+}
+
+// cp.async.wait_group takes an immediate: the few prefetch depths the host picks
+__device__ __forceinline__ void cp_async_wait_depth(int n) {
+  switch (n) {
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    case 3: cp_async_wait<3>(); break;
+    case 5: cp_async_wait<5>(); break;
+    case 7: cp_async_wait<7>(); break;
+    default: cp_async_wait<0>(); break;
+  }
+}
+
 template <int K>
 __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in, float* __restrict__ dst, Geometry g,
                                                   Taps t, Tiling tl) {
-  extern __shared__ __align__(16) unsigned char smem_floor[];  // residency cap only (see residency_floor)
-  (void)smem_floor;
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
   // channel varies fastest across CTAs: the channels of one pixel range run together and
   // share the interleaved lines in L2 (reads and partial-sector writes merge there)
@@ -700,11 +720,17 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const int D = tl.D;
+  const int PF = tl.pf;
+  int* lring = (int*)smem;          // [PF][HB][WS] lead bands
+  int* dring = lring + PF * HB * WS;  // [ndeep][PF][HB][WS] deep trail bands of boxes K-1, K-2, ...
   if (threadIdx.x < 32) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t tlane = tmem_base_s + ((uint32_t)(threadIdx.x & ~31) << 16);
+  bool deep[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) deep[i] = (2 * HB + t.pmax + t.p[i]) > D;  // trail older than the ring
 
   for (long long T = T0; T < T1;) {
     const int img = (int)(T / wh);
@@ -713,25 +739,27 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
     T = (long long)img * wh + (b - g.oy0);
     const int* mcol = mid_in + ch * g.mid_ch + (long long)img * g.mid_img + xc;
     const long long mrow = g.mid_row;
-    const uint64_t keep = l2_keep_policy();
-    // rows of one band, clamped only where the band crosses the image top or bottom
-    auto load_band = [&](int v0, uint32_t (&dst_)[HB]) {
+    // 16 rows from plane row v0 into ring band `slot` (rows clamped at the image edges)
+    auto fetch = [&](int* ring, int slot, int v0) {
+      int* sp = ring + slot * (HB * WS) + c;
       if (v0 >= 0 && v0 + HB <= g.H) {
         const int* p = mcol + (long long)v0 * mrow;
 #pragma unroll
         for (int r = 0; r < HB; ++r) {
-          dst_[r] = (uint32_t)ld_keep(p, keep);
+          cp_async4(sp + r * WS, p);
           p += mrow;
         }
       } else {
 #pragma unroll
-        for (int r = 0; r < HB; ++r)
-          dst_[r] = (uint32_t)ld_keep(mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow, keep);
+        for (int r = 0; r < HB; ++r) cp_async4(sp + r * WS, mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
       }
     };
     const int vstart = a - 1 - t.pmax;
     const int count = (b - a) + 2 * t.pmax + 1;
     const int nbands = (count + HB - 1) / HB;
+    const int nout = (b - a + HB - 1) / HB;
+    // output band ob is emitted at band iteration ob + W (full bands)
+    const int W = (2 * t.pmax + 1 + HB + HB - 1) / HB - 1;
     int box[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) box[i] = 0;
@@ -743,19 +771,30 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
       lead_s[i] = (t.pmax + 1 + t.p[i]) % D;
       trail_s[i] = (t.pmax - t.p[i]) % D;
     }
-    int out_next = a, prod_slot = 0;
-    uint32_t nxt[HB], nxt2[HB];  // two bands of look-ahead: loads overlap two bands of compute
-    load_band(vstart, nxt);
-    if (nbands > 1) load_band(vstart + HB, nxt2);
+    // one cp.async group per band iteration q: lead band q and the deep trails of output
+    // band q - W, issued PF - 1 iterations ahead
+    auto issue = [&](int q) {
+      if (q < nbands) fetch(lring, q % PF, vstart + q * HB);
+      const int ob = q - W;
+      if (ob >= 0 && ob < nout) {
+#pragma unroll
+        for (int d = 0; d < SB_NDEEP; ++d) {
+          const int i = K - 1 - d;
+          if (i >= 0 && d < tl.ndeep) fetch(dring + d * PF * HB * WS, ob % PF, a + ob * HB - t.p[i] - 1);
+        }
+      }
+      cp_async_commit();
+    };
+    for (int q = 0; q < PF - 1; ++q) issue(q);
+    int out_next = a, prod_slot = 0, ob = 0;
     for (int pb = 0; pb < nbands; ++pb) {
       const int n = min(HB, count - pb * HB);
+      issue(pb + PF - 1);
+      cp_async_wait_depth(PF - 1);  // lead band pb and the deep trails of output band pb - W landed
       uint32_t cur[HB];
+      const int* lp = lring + (pb % PF) * (HB * WS) + c;
 #pragma unroll
-      for (int r = 0; r < HB; ++r) {
-        cur[r] = nxt[r];
-        nxt[r] = nxt2[r];
-      }
-      if (pb + 2 < nbands) load_band(vstart + (pb + 2) * HB, nxt2);
+      for (int r = 0; r < HB; ++r) cur[r] = (uint32_t)lp[r * WS];
       tmem_st16(tlane + (uint32_t)prod_slot, cur);
       if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, cur);
       tmem_wait_st();
@@ -763,17 +802,26 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
       prod_slot += HB;
       prod_slot = prod_slot >= D ? 0 : prod_slot;
       if (produced >= 2 * t.pmax + 1 && produced - n < 2 * t.pmax + 1) {
-        for (int u = 0; u <= 2 * t.pmax; ++u) {
-          const int val = __ldg(mcol + (long long)min(max(vstart + u, 0), g.H - 1) * mrow);
-          const int au = u > t.pmax ? u - t.pmax : t.pmax - u;
+        // warm-up: the box sums of row a-1, 2*pmax+1 plane rows (L2-resident), 16 loads in flight
+        for (int u0 = 0; u0 <= 2 * t.pmax; u0 += HB) {
+          int val[HB];
 #pragma unroll
-          for (int i = 0; i < K; ++i)
-            if (au <= t.p[i]) box[i] += val;
+          for (int r = 0; r < HB; ++r)
+            val[r] = u0 + r <= 2 * t.pmax ? __ldg(mcol + (long long)min(max(vstart + u0 + r, 0), g.H - 1) * mrow) : 0;
+#pragma unroll
+          for (int r = 0; r < HB; ++r) {
+            const int u = u0 + r;
+            const int au = u > t.pmax ? u - t.pmax : t.pmax - u;
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+              if (u <= 2 * t.pmax && au <= t.p[i]) box[i] += val[r];
+          }
         }
       }
       while (out_next < b) {
         const int nb = min(HB, b - out_next);
         if (produced < (out_next - a) + nb + 2 * t.pmax + 1) break;
+        if (pb < ob + W) cp_async_wait_all();  // a short last band can be due before its group
         float ov[HB];
 #pragma unroll
         for (int r = 0; r < HB; ++r) ov[r] = 0.0f;
@@ -781,11 +829,20 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
         for (int i = 0; i < K; ++i) {
           uint32_t lv[HB], tv[HB];
           tmem_ld16(tlane + (uint32_t)lead_s[i], lv);
-          // the trail of row out_next is still in the ring iff D >= 2*HB + pmax + p_i
-          const bool trail_in_ring = (2 * HB + t.pmax + t.p[i]) <= D;
-          if (trail_in_ring) tmem_ld16(tlane + (uint32_t)trail_s[i], tv);
+          if (!deep[i]) tmem_ld16(tlane + (uint32_t)trail_s[i], tv);
           tmem_wait_ld();
-          if (!trail_in_ring) load_band(out_next - t.p[i] - 1, tv);
+          if (deep[i]) {
+            const int d = K - 1 - i;
+            if (d < tl.ndeep) {
+              const int* tp = dring + d * PF * HB * WS + (ob % PF) * (HB * WS) + c;
+#pragma unroll
+              for (int r = 0; r < HB; ++r) tv[r] = (uint32_t)tp[r * WS];
+            } else {
+              const int v0 = out_next - t.p[i] - 1;
+#pragma unroll
+              for (int r = 0; r < HB; ++r) tv[r] = (uint32_t)__ldg(mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
+            }
+          }
           int bx = box[i];
           const float w = t.w_col[i];
 #pragma unroll
@@ -810,8 +867,10 @@ __global__ void __launch_bounds__(WS) cols_kernel(const int* __restrict__ mid_in
           }
         }
         out_next += nb;
+        ++ob;
       }
     }
+    cp_async_wait_all();  // the segment's trailing (unused) groups
   }
   tmem_fence_before();
   __syncthreads();
