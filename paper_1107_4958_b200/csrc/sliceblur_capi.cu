@@ -148,7 +148,7 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
   tl.lanes_per_row = lpr;
   tl.stage_row_bytes = ceil16(tl.L * staged_ch * es);
   tl.ls = (m == sb::Mode::Fused) ? sb::LS : tl.L;
-  tl.packed = (m == sb::Mode::Fused && u8_single && ((tl.L + 63) & ~63) <= sb::LSP) ? 1 : 0;  // float2 prefixes
+  tl.packed = (m == sb::Mode::Fused && u8_single && ((tl.L + 63) & ~63) <= 192) ? 1 : 0;  // float2 prefixes
   if (tl.packed) {
     // the scan covers whole 64-column quarters; rows an odd multiple of 16 bytes apart
     tl.L = (tl.L + 63) & ~63;

@@ -47,8 +47,7 @@ constexpr int WS = 128;         // strip width = threads per CTA
 constexpr int NWARPS = WS / 32;
 constexpr int CH = 16;          // px per scan chunk (one lane)
 constexpr int LS = 512;         // prefix row stride in words (compile-time: immediate offsets)
-constexpr int LSP = 256;        // packed-prefix row stride in words (uint8, pmax <= 63)
-constexpr int LSP2 = LSP + 2;   // float2-prefix row stride: 2064 B = 16 (mod 128), conflict-free stores
+constexpr int LSP2 = 194;       // uint8 float2-prefix row stride (L <= 192): 1552 B = 16 (mod 128), conflict-free
 constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + kMagic rounds x to an integer (|x| < 2^22)
 constexpr int kMagicBits = 0x4B400000;  // bits(kMagic + n) = kMagicBits + n
 
@@ -367,54 +366,6 @@ __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restr
   if (bad && status) atomicOr(status, SB_STATUS_RANGE);
 }
 
-// uint8, one channel: rows q and q+8 of the band share P word q as two exact
-// 16-bit prefixes (L <= 256 staged bytes, so a prefix is at most 256*255 < 2^16
-// and is monotone: lead - trail never borrows across the fields).
-__device__ __forceinline__ void scan_rows_packed(const unsigned char* buf, uint32_t* __restrict__ P,
-                                                 const Tiling& tl, int warp = threadIdx.x >> 5,
-                                                 int nwarps = NWARPS) {
-  const int lane = threadIdx.x & 31;
-  const int lpr = tl.lanes_per_row;
-  const int pairs_per_warp = 32 / lpr;
-  const int sub = lane / lpr, sl = lane - sub * lpr;
-  const int nchunk = tl.L / CH;
-#pragma unroll 4
-  for (int q0 = warp * pairs_per_warp; q0 < HB / 2; q0 += nwarps * pairs_per_warp) {
-    const int q = q0 + sub;
-    const bool live = (q < HB / 2) && (sl < nchunk);
-    uint32_t v[CH];
-    uint32_t tot = 0;
-    if (live) {
-      const uint4 a = *(const uint4*)(buf + q * tl.stage_row_bytes + sl * CH);
-      const uint4 b = *(const uint4*)(buf + (q + HB / 2) * tl.stage_row_bytes + sl * CH);
-      const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
-      const uint32_t bw[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-      for (int m = 0; m < CH; ++m) {
-        // {a_m, 0, b_m, 0}: byte m of row q in field 0, of row q+8 in field 1
-        const uint32_t lo = __byte_perm(aw[m >> 2], 0u, 0x4440u | (m & 3));
-        const uint32_t hi = __byte_perm(bw[m >> 2], 0u, 0x4044u | ((m & 3) << 8));
-        tot = tot + lo + hi;
-        v[m] = tot;
-      }
-    }
-    uint32_t inc = tot;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      if (o >= lpr) break;
-      uint32_t y = __shfl_up_sync(0xffffffffu, inc, o, lpr);
-      if (sl >= o) inc += y;
-    }
-    const uint32_t carry = inc - tot;
-    if (live) {
-      uint4* dst = (uint4*)(P + q * LSP + sl * CH);
-#pragma unroll
-      for (int m = 0; m < CH / 4; ++m)
-        dst[m] = make_uint4(v[4 * m] + carry, v[4 * m + 1] + carry, v[4 * m + 2] + carry, v[4 * m + 3] + carry);
-    }
-  }
-}
-
 // uint8, one channel, float prefixes: rows q and q+8 of the band share float2 q of
 // P (x = row q, y = row q+8), stored as the fp32 numbers 2^23 + prefix.  For
 // 0 <= v < 2^23 the bit pattern of 2^23 + v is 0x4B000000 + v, so the scan is
@@ -423,8 +374,8 @@ __device__ __forceinline__ void scan_rows_packed(const unsigned char* buf, uint3
 // exact fp32 subtraction (FADD2 on a row pair) of two such values.
 // Lane = seg * 8 + q scans columns [seg*4*NW, (seg+1)*4*NW) of rows q and q+8;
 // the four segment offsets come from a two-step shuffle scan of packed 16-bit
-// totals (<= 256*255 < 2^16).  Staging rows are an odd multiple of 16 bytes
-// apart and P rows 2064 bytes, so each 8-lane phase of the 128-bit loads and
+// totals (<= 192*255 < 2^16).  Staging rows are an odd multiple of 16 bytes
+// apart and P rows 1552 bytes, so each 8-lane phase of the 128-bit loads and
 // stores touches 8 distinct bank groups.
 template <int NW>
 __device__ __forceinline__ void scan_rows_b2(const unsigned char* buf, float2* __restrict__ P, int srb) {
@@ -470,11 +421,10 @@ __device__ __forceinline__ void scan_rows_b2(const unsigned char* buf, float2* _
 
 __device__ __forceinline__ void scan_rows_b2_dispatch(const unsigned char* buf, float2* __restrict__ P,
                                                       const Tiling& tl) {
-  switch (tl.L >> 6) {  // packed tilings have L a multiple of 64, at most 256
+  switch (tl.L >> 6) {  // packed tilings have L a multiple of 64, at most 192
     case 1: scan_rows_b2<4>(buf, P, tl.stage_row_bytes); break;
     case 2: scan_rows_b2<8>(buf, P, tl.stage_row_bytes); break;
-    case 3: scan_rows_b2<12>(buf, P, tl.stage_row_bytes); break;
-    default: scan_rows_b2<16>(buf, P, tl.stage_row_bytes); break;
+    default: scan_rows_b2<12>(buf, P, tl.stage_row_bytes); break;
   }
 }
 
@@ -496,27 +446,6 @@ __device__ __forceinline__ void band_rows(const int* __restrict__ P, int c, cons
     const float wi = w[i];
 #pragma unroll
     for (int r = 0; r < HB; ++r) acc[r] = fmaf(wi, (float)(pl[r * ls] - pt[r * ls]), acc[r]);  // exact box sum
-  }
-}
-
-// Packed uint8 variant: word q holds rows q (bits 0-15) and q+8 (bits 16-31).
-template <int K>
-__device__ __forceinline__ void band_rows_packed(const uint32_t* __restrict__ P, int c, const Taps& t,
-                                                 const Tiling& tl, float (&acc)[HB]) {
-#pragma unroll
-  for (int r = 0; r < HB; ++r) acc[r] = 0.0f;
-  const int base = c + tl.xoff;
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    const uint32_t* pl = P + base + t.p[i];
-    const uint32_t* pt = P + base - t.p[i] - 1;
-    const float wl = t.w_row[i];
-#pragma unroll
-    for (int q = 0; q < HB / 2; ++q) {
-      const uint32_t d = pl[q * LSP] - pt[q * LSP];  // two exact 16-bit box sums
-      acc[q] = fmaf(wl, i2f_fast(d & 0xFFFFu), acc[q]);
-      acc[q + HB / 2] = fmaf(wl, i2f_fast(d >> 16), acc[q + HB / 2]);
-    }
   }
 }
 
@@ -918,7 +847,7 @@ __global__ void __launch_bounds__(FTHREADS, 2)
   const int pbuf_words = packed ? HB * LSP2 : HB * LS;  // packed: HB/2 float2 rows
   unsigned char* stage = smem;                                        // FPROD producers x 2 staged bands
   int* Pbase = (int*)(smem + 2 * FPROD * HB * tl.stage_row_bytes);    // FPROD x npb prefix buffers
-  // FCONS x 2 output bands (TMA stores; 128-byte aligned shared addresses)
+  // FCONS x 2 output bands of HB x 32 floats (TMA stores; 128-byte aligned shared addresses)
   float* obuf = (float*)(smem + (((smem_u32(smem) + tl.obuf_off + 127u) & ~127u) - smem_u32(smem)));
   const int D = tl.D;
 
