@@ -181,6 +181,8 @@ size_t residency_floor(int ctas) { return 233472 / (size_t)(ctas + 1) - 1024 + 1
 size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
   if (m == sb::Mode::ColsFromMid)
     return std::max((size_t)(1 + tl.ndeep) * tl.pf * sb::HB * sb::WS * sizeof(int), residency_floor(512 / tl.tmem_cols));
+  if (m == sb::Mode::ColsPrefix)  // plane ring + band copies + output boxes (TMA stores)
+    return (size_t)tl.obuf_off + 128 + (size_t)4 * sb::CG * 2 * sb::HB * 32 * sizeof(float);
   if (m == sb::Mode::Fused) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
     // + FCONS x 2 output bands of HB x 32 floats staged for TMA tensor stores
@@ -211,6 +213,40 @@ const void* pick_kernel(sb::Mode m, int dtype, int k) {
 // row ranges of the tall (batch*H) image; items is sized so the grid fills the
 // GPU about once, but never so small that the 2*pmax+1 warm-up rows of a
 // column sweep exceed ~1/8 of the rows it outputs.
+// Tiling of the prefix-form column kernel (cols2_kernel): a 496-row TMEM ring,
+// CG output groups, trail windows classified as ring or band copies.  False when
+// a window would straddle the two (the running-sum cols_kernel is used then).
+bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int pmax, sb::Tiling* out) {
+  sb::Tiling tl = base;
+  const int NB = 31;
+  tl.D = NB * sb::HB;
+  tl.tmem_cols = 512;
+  const int span = 2 + pmax / 8;               // ring bands one output band reads
+  tl.lag = span + sb::CG - 1;
+  const int thr = span + sb::CG - 2 - NB;      // bands at offset <= thr come from the copies
+  tl.deepmask = 0;
+  for (int i = 0; i < k; ++i) {
+    const int off = pmax - (int)radii[i];
+    const int lo = off / sb::HB, hi = (off + sb::HB - 1) / sb::HB;
+    if (hi <= thr) tl.deepmask |= 1 << i;
+    else if (lo <= thr) return false;          // straddles the copies and the ring
+    if ((pmax + 1 + (int)radii[i]) / sb::HB <= thr) return false;  // leads always from the ring
+  }
+  tl.ds = tl.deepmask ? thr + sb::CG + 1 : 0;
+  const size_t band = (size_t)sb::HB * sb::WS * sizeof(int);
+  const size_t obuf = (size_t)4 * sb::CG * 2 * sb::HB * 32 * sizeof(float) + 128;
+  tl.pf = 0;
+  for (int pf : {8, 6, 4, 3, 2})
+    if ((size_t)(pf + tl.ds) * band + obuf <= kSmemBudget) {
+      tl.pf = pf;
+      break;
+    }
+  if (!tl.pf) return false;
+  tl.obuf_off = (int)((size_t)(tl.pf + tl.ds) * band);
+  *out = tl;
+  return true;
+}
+
 int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, int W, long long total_rows,
                 int channels, Launch* out) {
   sb::Tiling& tl = out->tl;
@@ -233,15 +269,16 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, in
   int smem_per_sm = 233472, regs_per_sm = 65536;
   cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   cudaDeviceGetAttribute(&regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-  const int threads = (m == sb::Mode::Fused) ? sb::FTHREADS : sb::WS;
+  const int threads = (m == sb::Mode::Fused) ? sb::FTHREADS : (m == sb::Mode::ColsPrefix ? sb::C2THREADS : sb::WS);
   const int regs_per_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (threads / 32);
   occ = std::min(2048 / threads, regs_per_sm / std::max(1, regs_per_cta));
   occ = std::min<long long>(occ, (long long)smem_per_sm / (long long)(smem + fa.sharedSizeBytes + 1024));
-  if (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid) occ = std::min(occ, 512 / tl.tmem_cols);
+  if (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid || m == sb::Mode::ColsPrefix)
+    occ = std::min(occ, 512 / tl.tmem_cols);
   occ = std::max(occ, 1);
   const long long slots = (long long)sms * occ;
   const long long columns = (long long)tl.nstrips * channels;
-  const bool sweeps = (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid);
+  const bool sweeps = (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid || m == sb::Mode::ColsPrefix);
   // Column sweeps pay 2*pmax+1 warm-up rows per item; the row pass pays nothing.
   // Pick the item count minimising (waves of CTAs) x (rows per item incl. warm-up).
   const long long warm = sweeps ? 2LL * pmax + 1 : 0;
@@ -477,6 +514,21 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
         ct.pf = pf;
         break;
       }
+  }
+  sb::Tiling pt;
+  if (getenv("SB_NO_COLS2") == nullptr && cols_prefix_tiling(ct, radii, k, plan.pmax, &pt)) {
+    const void* f3 = sb::sweep_ptr_cols2(k);
+    Launch L3;
+    rc = plan_launch(f3, sb::Mode::ColsPrefix, pt, plan.pmax, g.W, total_rows, channels, &L3);
+    if (rc) return rc;
+    sb::Geometry g2 = g;
+    alignas(64) CUtensorMap omap;
+    make_output_map(dst, g2, &omap);
+    void* args[] = {(void*)&mid, (void*)&dst, (void*)&g2, (void*)&plan.taps, (void*)&L3.tl, (void*)&omap};
+    // channels are folded into grid.x (fastest varying), as in cols_kernel
+    cudaError_t e = cudaLaunchKernel(f3, dim3(L3.grid.x * L3.grid.y), dim3(sb::C2THREADS), args, L3.smem, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+    return SB_OK;
   }
   rc = plan_launch(f2, sb::Mode::ColsFromMid, ct, plan.pmax, g.W, total_rows, channels, &L2);
   if (rc) return rc;

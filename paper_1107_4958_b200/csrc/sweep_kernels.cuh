@@ -91,9 +91,12 @@ struct Tiling {
   int obuf_off;         // fused: byte offset of the output staging bands in shared memory
   int pf;               // cols: plane bands prefetched ahead (2, 3, 4, 6 or 8)
   int ndeep;            // cols: largest boxes whose trails are re-read from the plane (0..SB_NDEEP)
+  int ds;               // cols2: ring-band copies kept in shared memory (0 = none)
+  int deepmask;         // cols2: bit i = box i's trail window is read from the copies
+  int lag;              // cols2: ring band v is written once output band v - lag is done
 };
 
-enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3 };
+enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3, ColsPrefix = 4 };
 
 // ---------------------------------------------------------------- small helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1037,6 +1040,256 @@ __global__ void __launch_bounds__(FTHREADS, 2)
   if (warp == 0) tmem_dealloc(tmem_base_s, (uint32_t)tl.tmem_cols);
 }
 
+// The segments of one CTA's row range: every image the range touches restarts
+// its sweep (virtual rows a-1-pmax .. b-1+pmax of output rows [a, b)); gb0 is
+// the global index of the segment's first 16-row band.
+struct SegIter {
+  long long T, T1, wh;
+  int oy0, pmax;
+  int img, a, b, count, nbands;
+  uint32_t gb0;
+  bool valid;
+  __device__ __forceinline__ void init(long long T0_, long long T1_, long long wh_, int oy0_, int pmax_) {
+    T = T0_, T1 = T1_, wh = wh_, oy0 = oy0_, pmax = pmax_, gb0 = 0, nbands = 0;
+    load();
+  }
+  __device__ __forceinline__ void load() {
+    valid = T < T1;
+    if (!valid) return;
+    img = (int)(T / wh);
+    a = oy0 + (int)(T - (long long)img * wh);
+    b = oy0 + (int)min(wh, T1 - (long long)img * wh);
+    count = (b - a) + 2 * pmax + 1;
+    nbands = (count + HB - 1) / HB;
+  }
+  __device__ __forceinline__ void next() {
+    T = (long long)img * wh + (b - oy0);
+    gb0 += (uint32_t)nbands;
+    load();
+  }
+};
+constexpr int FRING = 32;  // max ring slots (512 TMEM columns / HB)
+
+// ---------------------------------------------------------------- column pass, prefix form (large radii)
+// ColsFromMid with independent output bands: one CTA per strip and SM, the ring
+// in TMEM holds the running column PREFIX C of the R plane (as in the fused
+// kernel), so every output band is C(y+p) - C(y-p-1) windows with no running
+// state and CG output warp groups emit bands j = g (mod CG) concurrently.
+//  * loader warps (4, one per TMEM lane quadrant): plane rows arrive through a
+//    cp.async ring tl.pf bands ahead; the loader accumulates C and appends each
+//    band to the ring after every output band that reads the overwritten band
+//    from TMEM is done (lag tl.lag = span + CG - 1 bands);
+//  * trails older than the ring (C5's largest box) are read from a shared-memory
+//    copy: the loader copies band u = v - NB + CG - 1 out of TMEM while writing
+//    band v, so it is there before any output band needs it and stays there for
+//    tl.ds bands.  The host classifies every trail window as ring or copy
+//    (tl.deepmask) and falls back to cols_kernel when a window would straddle.
+constexpr int CG = 3;                          // output warp groups
+constexpr int C2THREADS = 32 * 4 * (1 + CG);   // loader group + CG output groups
+constexpr int C2DONE = 8;                      // output-band done barriers (> CG)
+
+template <int K>
+__global__ void __launch_bounds__(C2THREADS, 1)
+    cols2_kernel(const int* __restrict__ mid_in, float* __restrict__ dst, Geometry g, Taps t, Tiling tl,
+                 const __grid_constant__ CUtensorMap omap) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ __align__(8) uint64_t full[FRING], done[C2DONE];
+  const int ch = blockIdx.x % g.in_px;
+  const int sidx = blockIdx.x / g.in_px;
+  const int strip = sidx % tl.nstrips;
+  const long long item = sidx / tl.nstrips;
+  const int x0 = strip * WS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3;  // TMEM lane quadrant: columns 32q .. 32q+31
+  const int c = 32 * q + lane;
+  const int xc = (x0 + c) < g.W ? x0 + c : g.W - 1;  // inactive lanes mirror a valid column (no stores)
+  const int wh = g.oy1 - g.oy0;
+  const long long total = (long long)g.nimg * wh;
+  const long long T0 = item * tl.rows_per_item;
+  const long long T1 = min(T0 + tl.rows_per_item, total);
+  const int D = tl.D, NB = D / HB, PF = tl.pf, DS = tl.ds;
+  int* lring = (int*)smem;                    // [PF][HB][WS] plane bands (cp.async)
+  int* dring = lring + PF * HB * WS;          // [DS][HB][WS] copies of old ring bands
+  float* obuf = (float*)(smem + (((smem_u32(smem) + tl.obuf_off + 127u) & ~127u) - smem_u32(smem)));
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NB; ++i) mbar_init(&full[i], 32 * 4);
+    for (int i = 0; i < C2DONE; ++i) mbar_init(&done[i], 32 * 4);
+  }
+  if (warp == 0) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tlane = tmem_base_s + ((uint32_t)q << 21);
+
+  if (warp < 4) {
+    // ------------------------------------------------ loader
+    SegIter sc, so;  // ring bands / the output bands whose completion gates the ring
+    sc.init(T0, T1, wh, g.oy0, t.pmax);
+    so.init(T0, T1, wh, g.oy0, t.pmax);
+    uint32_t v = 0;  // global ring band
+    uint32_t onum = 0;
+    int oob = 0;     // next output band to observe: index onum, band oob of segment so
+    int slot = 0;
+    for (; sc.valid; sc.next()) {
+      const int* mcol = mid_in + ch * g.mid_ch + (long long)sc.img * g.mid_img + xc;
+      const long long mrow = g.mid_row;
+      const int vstart = sc.a - 1 - t.pmax;
+      auto issue = [&](int pb) {
+        if (pb < sc.nbands) {
+          int* sp = lring + (pb % PF) * (HB * WS) + c;
+          const int v0 = vstart + pb * HB;
+#pragma unroll
+          for (int r = 0; r < HB; ++r) cp_async4(sp + r * WS, mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
+        }
+        cp_async_commit();
+      };
+      for (int pb = 0; pb < PF - 1; ++pb) issue(pb);
+      int cprefix = 0;
+      for (int pb = 0; pb < sc.nbands; ++pb, ++v) {
+        issue(pb + PF - 1);
+        // every output band reading ring band v - NB from TMEM is done
+        while (so.valid && (long long)(so.gb0 + (uint32_t)oob) + tl.lag <= (long long)v) {
+          mbar_wait(&done[onum % C2DONE], (onum / C2DONE) & 1);
+          ++onum;
+          if (++oob == (so.b - so.a + HB - 1) / HB) {
+            so.next();
+            oob = 0;
+          }
+        }
+        if (DS > 0) {
+          // copy band u out of the ring before it is overwritten (see above)
+          const long long u = (long long)v - NB + CG - 1;
+          if (u >= 0) {
+            uint32_t old[HB];
+            tmem_ld16(tlane + (uint32_t)((u % NB) * HB), old);
+            tmem_wait_ld();
+            int* dp = dring + (int)(u % DS) * (HB * WS) + c;
+#pragma unroll
+            for (int r = 0; r < HB; ++r) dp[r * WS] = (int)old[r];
+          }
+        }
+        cp_async_wait_depth(PF - 1);
+        const int* lp = lring + (pb % PF) * (HB * WS) + c;
+        uint32_t cv[HB];
+#pragma unroll
+        for (int r = 0; r < HB; ++r) {
+          cprefix += lp[r * WS];
+          cv[r] = (uint32_t)cprefix;
+        }
+        tmem_st16(tlane + (uint32_t)(slot * HB), cv);
+        if (slot == 0) tmem_st16(tlane + (uint32_t)D, cv);  // mirror: lag windows never wrap
+        tmem_wait_st();
+        tmem_fence_before();
+        mbar_arrive(&full[slot]);
+        if (++slot == NB) slot = 0;
+      }
+      cp_async_wait_all();
+    }
+  } else {
+    // ------------------------------------------------ output groups
+    const int grp = warp / 4 - 1;
+    const int ow = warp - 4;  // output warp 0 .. 4*CG-1 (staging buffers)
+    uint32_t ready = 0;       // ring bands observed full
+    int rslot = 0;
+    uint32_t rph = 0;
+    uint32_t onum = 0;
+    int obsel = 0;
+    SegIter so;
+    so.init(T0, T1, wh, g.oy0, t.pmax);
+    for (; so.valid; so.next()) {
+      const int nout = (so.b - so.a + HB - 1) / HB;
+      for (int ob = 0; ob < nout; ++ob, ++onum) {
+        if ((int)(onum % CG) != grp) continue;
+        const int out_next = so.a + ob * HB;
+        const int nb = min(HB, so.b - out_next);
+        const uint32_t j = so.gb0 + (uint32_t)ob;  // ring band of the band's deepest trail row
+        const uint32_t need = so.gb0 + (uint32_t)((ob * HB + nb + 2 * t.pmax) / HB);
+        while (ready <= need) {
+          mbar_wait(&full[rslot], rph);
+          if (++rslot == NB) {
+            rslot = 0;
+            rph ^= 1;
+          }
+          ++ready;
+        }
+        tmem_fence_after();
+        const int base = (int)(j % (uint32_t)NB) * HB;  // ring position of virtual row 16*ob
+        float2 o2[HB / 2];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          uint32_t lv[HB], tv[HB];
+          int l = base + t.pmax + 1 + t.p[i];
+          l = l >= D ? l - D : l;
+          l = l >= D ? l - D : l;
+          tmem_ld16(tlane + (uint32_t)l, lv);
+          const bool deep = (tl.deepmask >> i) & 1;
+          if (!deep) {
+            int tr = base + t.pmax - t.p[i];
+            tr = tr >= D ? tr - D : tr;
+            tmem_ld16(tlane + (uint32_t)tr, tv);
+          }
+          tmem_wait_ld();
+          if (deep) {
+            // virtual rows 16*ob + pmax - p_i .. +15 from the band copies (band j + off/16 on)
+            const int off = t.pmax - t.p[i];
+            const uint32_t u0 = j + (uint32_t)(off / HB);
+            const int r0 = off % HB;
+#pragma unroll
+            for (int r = 0; r < HB; ++r) {
+              const int rr = r0 + r;
+              const uint32_t u = u0 + (uint32_t)(rr >= HB);
+              tv[r] = (uint32_t)dring[(int)(u % (uint32_t)DS) * (HB * WS) + (rr & (HB - 1)) * WS + c];
+            }
+          }
+          const float2 w2 = make_float2(t.w_col[i], t.w_col[i]);
+#pragma unroll
+          for (int r = 0; r < HB / 2; ++r) {
+            const float2 d = make_float2(i2f_fast(lv[2 * r] - tv[2 * r]), i2f_fast(lv[2 * r + 1] - tv[2 * r + 1]));
+            o2[r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, o2[r]);
+          }
+        }
+        tmem_fence_before();
+        mbar_arrive(&done[onum % C2DONE]);
+        if (g.out_bulk && nb == HB) {
+          float* obp = obuf + (ow * 2 + obsel) * (HB * 32);
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+#pragma unroll
+          for (int r = 0; r < HB / 2; ++r) {
+            obp[(2 * r) * 32 + lane] = o2[r].x;
+            obp[(2 * r + 1) * 32 + lane] = o2[r].y;
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&omap, obp, x0 + 32 * q, out_next - g.oy0, so.img);
+            bulk_commit();
+          }
+          obsel ^= 1;
+        } else if (x0 + c < g.W) {
+          float* dptr = dst + (long long)so.img * g.out_img + (long long)(out_next - g.oy0) * g.out_row +
+                        (long long)(x0 + c) * g.out_px + ch;
+          const long long step = g.out_row;
+#pragma unroll
+          for (int r = 0; r < HB / 2; ++r) {
+            if (2 * r < nb) st_stream(dptr, o2[r].x);
+            dptr += step;
+            if (2 * r + 1 < nb) st_stream(dptr, o2[r].y);
+            dptr += step;
+          }
+        }
+      }
+    }
+    // observe the remaining ring bands so no full phase is left pending (not needed for
+    // correctness: the CTA ends here) and retire the stores
+    if (lane == 0) bulk_wait_read<0>();
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem_base_s, (uint32_t)tl.tmem_cols);
+}
+
 // ---------------------------------------------------------------- streaming row pass (large radii)
 // RowsToMid for radii too large for the fused sweep.  A CTA owns a band of HB
 // rows and streams its full width in chunks of CW columns, so the 2*pmax+1
@@ -1229,7 +1482,8 @@ const void* sweep_ptr_u8(Mode m, int k);
 const void* sweep_ptr_u16(Mode m, int k);
 const void* sweep_ptr_f32(Mode m, int k);
 const void* sweep_ptr_f64(Mode m, int k);
-const void* sweep_ptr_cols(int k);  // ColsFromMid (source type unused)
+const void* sweep_ptr_cols(int k);   // ColsFromMid (source type unused)
+const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)
 
 template <typename Tin>
@@ -1264,6 +1518,12 @@ inline const void* cols_ptr_for(int k) {
 #define SB_COLS(KK) cols_kernel<KK>
   SB_K_CASES(SB_COLS)
 #undef SB_COLS
+}
+
+inline const void* cols2_ptr_for(int k) {
+#define SB_COLS2(KK) cols2_kernel<KK>
+  SB_K_CASES(SB_COLS2)
+#undef SB_COLS2
 #undef SB_K_CASES
 }
 

@@ -4,12 +4,11 @@
 cfg=$1; shift
 for rep in 1 2; do
 for lib in "$@"; do
-  unset SB_LIB_PATH SB_NO_TMA_STORE
   case "$lib" in
-    default) ;;
-    env:*) export "${lib#env:}" ;;
-    *) export SB_LIB_PATH=$PWD/$lib ;;
+    default) envs="" ;;
+    env:*) envs="${lib#env:}" ;;
+    *) envs="SB_LIB_PATH=$PWD/$lib" ;;
   esac
-  v=$(timeout 200 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print(d['ms_per_step'], d['value'], d.get('parity',{}).get('max_abs'))")
+  v=$(env $envs timeout 200 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print(d['ms_per_step'], d['value'], d.get('parity',{}).get('max_abs'))")
   echo "$cfg $lib rep$rep: $v"
 done; done
