@@ -221,30 +221,43 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
   const int NB = 31;
   tl.D = NB * sb::HB;
   tl.tmem_cols = 512;
-  const int span = 2 + pmax / 8;               // ring bands one output band reads
-  tl.lag = span + sb::CG - 1;
-  const int thr = span + sb::CG - 2 - NB;      // bands at offset <= thr come from the copies
-  tl.deepmask = 0;
-  for (int i = 0; i < k; ++i) {
-    const int off = pmax - (int)radii[i];
-    const int lo = off / sb::HB, hi = (off + sb::HB - 1) / sb::HB;
-    if (hi <= thr) tl.deepmask |= 1 << i;
-    else if (lo <= thr) return false;          // straddles the copies and the ring
-    if ((pmax + 1 + (int)radii[i]) / sb::HB <= thr) return false;  // leads always from the ring
-  }
-  tl.ds = tl.deepmask ? thr + sb::CG + 1 : 0;
   const size_t band = (size_t)sb::HB * sb::WS * sizeof(int);
   const size_t obuf = (size_t)4 * sb::CG * 2 * sb::HB * 32 * sizeof(float) + 128;
-  tl.pf = 0;
-  for (int pf : {8, 6, 4, 3, 2})
-    if ((size_t)(pf + tl.ds) * band + obuf <= kSmemBudget) {
-      tl.pf = pf;
-      break;
+  const int span = 2 + pmax / 8;  // ring bands one output band reads
+  // Slack: bands the loader may run ahead of the output groups.  Without band copies the
+  // ring bounds it (lag <= NB); with copies, each slack band costs two copy slots.
+  int slack = NB - span - sb::CG + 1;
+  if (slack < 0) slack = 3;
+  for (; slack >= 0; --slack) {
+    tl.lag = span + sb::CG - 1 + slack;
+    tl.copy_e = tl.lag - span;
+    // output band o + C2DONE may finish before the loader observed band o's done phase
+    // unless the loader has passed o by then: C2DONE >= lag - span + 1
+    if (tl.lag - span + 1 > sb::C2DONE) continue;
+    const int thr = tl.lag - 1 - NB;  // bands at offset <= thr come from the copies
+    tl.deepmask = 0;
+    bool ok = true;
+    for (int i = 0; i < k && ok; ++i) {
+      const int off = pmax - (int)radii[i];
+      const int lo = off / sb::HB, hi = (off + sb::HB - 1) / sb::HB;
+      if (hi <= thr) tl.deepmask |= 1 << i;
+      else if (lo <= thr) ok = false;                               // straddles copies and ring
+      if ((pmax + 1 + (int)radii[i]) / sb::HB <= thr) ok = false;   // leads always from the ring
     }
-  if (!tl.pf) return false;
-  tl.obuf_off = (int)((size_t)(tl.pf + tl.ds) * band);
-  *out = tl;
-  return true;
+    if (!ok) continue;
+    tl.ds = thr >= 0 ? 2 * tl.lag - NB - span + 1 : 0;
+    tl.pf = 0;
+    for (int pf : {8, 6, 4, 3, 2})
+      if ((size_t)(pf + tl.ds) * band + obuf <= kSmemBudget) {
+        tl.pf = pf;
+        break;
+      }
+    if (!tl.pf) continue;
+    tl.obuf_off = (int)((size_t)(tl.pf + tl.ds) * band);
+    *out = tl;
+    return true;
+  }
+  return false;
 }
 
 int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, int W, long long total_rows,
@@ -516,7 +529,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
       }
   }
   sb::Tiling pt;
-  if (getenv("SB_NO_COLS2") == nullptr && cols_prefix_tiling(ct, radii, k, plan.pmax, &pt)) {
+  if (cols_prefix_tiling(ct, radii, k, plan.pmax, &pt)) {
     const void* f3 = sb::sweep_ptr_cols2(k);
     Launch L3;
     rc = plan_launch(f3, sb::Mode::ColsPrefix, pt, plan.pmax, g.W, total_rows, channels, &L3);

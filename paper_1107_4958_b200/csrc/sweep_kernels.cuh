@@ -94,6 +94,7 @@ struct Tiling {
   int ds;               // cols2: ring-band copies kept in shared memory (0 = none)
   int deepmask;         // cols2: bit i = box i's trail window is read from the copies
   int lag;              // cols2: ring band v is written once output band v - lag is done
+  int copy_e;           // cols2: band v - D/HB + copy_e is copied out of the ring while band v is written
 };
 
 enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3, ColsPrefix = 4 };
@@ -1079,14 +1080,15 @@ constexpr int FRING = 32;  // max ring slots (512 TMEM columns / HB)
 //    cp.async ring tl.pf bands ahead; the loader accumulates C and appends each
 //    band to the ring after every output band that reads the overwritten band
 //    from TMEM is done (lag tl.lag = span + CG - 1 bands);
-//  * trails older than the ring (C5's largest box) are read from a shared-memory
-//    copy: the loader copies band u = v - NB + CG - 1 out of TMEM while writing
+//  * trails older than the ring (C5's largest boxes) are read from a shared-memory
+//    copy: the loader copies band u = v - NB + tl.copy_e out of TMEM while writing
 //    band v, so it is there before any output band needs it and stays there for
-//    tl.ds bands.  The host classifies every trail window as ring or copy
+//    tl.ds bands (copy_e = lag - span lets the loader run lag - span - CG + 1
+//    bands of slack ahead of the output groups).  The host classifies every trail window as ring or copy
 //    (tl.deepmask) and falls back to cols_kernel when a window would straddle.
 constexpr int CG = 3;                          // output warp groups
 constexpr int C2THREADS = 32 * 4 * (1 + CG);   // loader group + CG output groups
-constexpr int C2DONE = 8;                      // output-band done barriers (> CG)
+constexpr int C2DONE = 32;  // output-band done barriers: >= lag - span + 1, so no barrier is lapped
 
 template <int K>
 __global__ void __launch_bounds__(C2THREADS, 1)
@@ -1139,8 +1141,17 @@ __global__ void __launch_bounds__(C2THREADS, 1)
         if (pb < sc.nbands) {
           int* sp = lring + (pb % PF) * (HB * WS) + c;
           const int v0 = vstart + pb * HB;
+          if (v0 >= 0 && v0 + HB <= g.H) {
+            const int* gp = mcol + (long long)v0 * mrow;
 #pragma unroll
-          for (int r = 0; r < HB; ++r) cp_async4(sp + r * WS, mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
+            for (int r = 0; r < HB; ++r) {
+              cp_async4(sp + r * WS, gp);
+              gp += mrow;
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < HB; ++r) cp_async4(sp + r * WS, mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
+          }
         }
         cp_async_commit();
       };
@@ -1159,7 +1170,7 @@ __global__ void __launch_bounds__(C2THREADS, 1)
         }
         if (DS > 0) {
           // copy band u out of the ring before it is overwritten (see above)
-          const long long u = (long long)v - NB + CG - 1;
+          const long long u = (long long)v - NB + tl.copy_e;
           if (u >= 0) {
             uint32_t old[HB];
             tmem_ld16(tlane + (uint32_t)((u % NB) * HB), old);
@@ -1235,11 +1246,18 @@ __global__ void __launch_bounds__(C2THREADS, 1)
             const int off = t.pmax - t.p[i];
             const uint32_t u0 = j + (uint32_t)(off / HB);
             const int r0 = off % HB;
+            const int s0 = (int)(u0 % (uint32_t)DS);
+            const int* p0 = dring + s0 * (HB * WS) + c;
+            if (r0 == 0) {
 #pragma unroll
-            for (int r = 0; r < HB; ++r) {
-              const int rr = r0 + r;
-              const uint32_t u = u0 + (uint32_t)(rr >= HB);
-              tv[r] = (uint32_t)dring[(int)(u % (uint32_t)DS) * (HB * WS) + (rr & (HB - 1)) * WS + c];
+              for (int r = 0; r < HB; ++r) tv[r] = (uint32_t)p0[r * WS];
+            } else {
+              const int* p1 = dring + (s0 + 1 == DS ? 0 : s0 + 1) * (HB * WS) + c;
+#pragma unroll
+              for (int r = 0; r < HB; ++r) {
+                const int rr = r0 + r;
+                tv[r] = (uint32_t)(rr < HB ? p0[rr * WS] : p1[(rr - HB) * WS]);
+              }
             }
           }
           const float2 w2 = make_float2(t.w_col[i], t.w_col[i]);
