@@ -16,6 +16,14 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a); run with -m gpu")
 
 
+def pytest_collection_modifyitems(config, items):
+    # a kernel that never finishes must end the run, not stall it: GPU tests get a
+    # thread-method timeout (dumps the stacks and exits) unless they set their own
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(240, method="thread"))
+
+
 @pytest.fixture(scope="session")
 def golden_cases():
     import numpy as np

@@ -301,3 +301,29 @@ def test_kernel_too_large_and_1d_edges():
     # single-pixel image with a p = 0 kernel is the identity
     one = np.array([[42.0]], np.float32)
     assert F.separable_filter_2d(one, A.SliceKernel((0,), (1.0,)))[0, 0] == pytest.approx(42.0, abs=BAR)
+
+
+@pytest.mark.parametrize("shape,k,sigma,ch,batch", [
+    ((700, 300), 4, 100.0, 1, 1),   # pmax 257: band copies for the largest box
+    ((600, 520), 5, 64.0, 3, 1),    # pmax 170, interleaved channels: ring only
+    ((400, 260), 3, 40.0, 1, 3),    # a batch: segments of several images per CTA
+    ((1100, 250), 4, 75.0, 1, 2),   # tall narrow images, two strips
+    ((520, 530), 5, 90.0, 2, 1),
+])
+def test_two_launch_path_configs(shape, k, sigma, ch, batch):
+    # the large-radius path (row plane + prefix-form column kernel) on shapes that
+    # exercise its ring / band-copy classification and multi-segment items
+    rng = np.random.default_rng(int(sigma) * 7 + k)
+    kern = A.table_kernel(k, sigma)
+    h, w = shape
+    if kern.radii[-1] >= min(h, w):
+        pytest.skip("kernel larger than the image")
+    x = (rng.random((batch, h, w, ch) if ch > 1 else (batch, h, w)) * 255).astype(np.float32)
+    got = F.separable_filter_batch(x, kern, channels_last=ch > 1, value_bound=255.0)
+    for bi in range(batch):
+        for c in range(ch):
+            img = x[bi, :, :, c] if ch > 1 else x[bi]
+            ref = O.separable_filter_2d(np.ascontiguousarray(img, np.float64), kern.radii, kern.weights)
+            res = got[bi, :, :, c] if ch > 1 else got[bi]
+            err = np.abs(res - ref)
+            assert err.max() <= BAR, (shape, k, sigma, ch, batch, float(err.max()))
