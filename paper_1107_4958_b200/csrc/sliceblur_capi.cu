@@ -181,7 +181,7 @@ size_t residency_floor(int ctas) { return 233472 / (size_t)(ctas + 1) - 1024 + 1
 size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
   if (m == sb::Mode::ColsFromMid)
     return std::max((size_t)(1 + tl.ndeep) * tl.pf * sb::HB * sb::WS * sizeof(int), residency_floor(512 / tl.tmem_cols));
-  if (m == sb::Mode::ColsPrefix)  // plane ring + band copies + output boxes (TMA stores)
+  if (m == sb::Mode::ColsPrefix)  // plane ring + band copies + output boxes (TMA), 128-byte aligned
     return (size_t)tl.obuf_off + 128 + (size_t)4 * sb::CG * 2 * sb::HB * 32 * sizeof(float);
   if (m == sb::Mode::Fused) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
@@ -247,7 +247,7 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
     if (!ok) continue;
     tl.ds = thr >= 0 ? 2 * tl.lag - NB - span + 1 : 0;
     tl.pf = 0;
-    for (int pf : {8, 6, 4, 3, 2})
+    for (int pf : {sb::C2PF, 6, 4, 3, 2})
       if ((size_t)(pf + tl.ds) * band + obuf <= kSmemBudget) {
         tl.pf = pf;
         break;
@@ -375,6 +375,22 @@ void make_output_map(float* dst, sb::Geometry& g, CUtensorMap* map) {
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     g.out_bulk = 0;
+}
+
+// Tensor map of the int32 R plane [channel*batch][H][W] with a 16 x 128 box (the
+// prefix-form column kernel loads one band per TMA).  False when the plane rows
+// are not 16-byte multiples or no map can be made.
+bool make_plane_map(const int* mid, const sb::Geometry& g, int channels, CUtensorMap* map) {
+  std::memset(map, 0, sizeof(*map));
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc || (g.mid_row * 4) % 16 != 0 || (g.mid_img * 4) % 16 != 0 || (uintptr_t)mid % 16 != 0) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.nimg * (cuuint64_t)channels};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.mid_row * 4, (cuuint64_t)g.mid_img * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)sb::WS, (cuuint32_t)sb::HB, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, (void*)mid, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
 }
 
 int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, const sb::Geometry& g0,
@@ -529,7 +545,8 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
       }
   }
   sb::Tiling pt;
-  if (cols_prefix_tiling(ct, radii, k, plan.pmax, &pt)) {
+  alignas(64) CUtensorMap mmap;
+  if (make_plane_map(mid, g, channels, &mmap) && cols_prefix_tiling(ct, radii, k, plan.pmax, &pt)) {
     const void* f3 = sb::sweep_ptr_cols2(k);
     Launch L3;
     rc = plan_launch(f3, sb::Mode::ColsPrefix, pt, plan.pmax, g.W, total_rows, channels, &L3);
@@ -537,7 +554,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     sb::Geometry g2 = g;
     alignas(64) CUtensorMap omap;
     make_output_map(dst, g2, &omap);
-    void* args[] = {(void*)&mid, (void*)&dst, (void*)&g2, (void*)&plan.taps, (void*)&L3.tl, (void*)&omap};
+    void* args[] = {(void*)&mid, (void*)&dst, (void*)&g2, (void*)&plan.taps, (void*)&L3.tl, (void*)&omap, (void*)&mmap};
     // channels are folded into grid.x (fastest varying), as in cols_kernel
     cudaError_t e = cudaLaunchKernel(f3, dim3(L3.grid.x * L3.grid.y), dim3(sb::C2THREADS), args, L3.smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");

@@ -131,6 +131,16 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
                "r"(smem_u32(ssrc)), "r"(x), "r"(y), "r"(z)
                : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* sdst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(sdst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -1076,8 +1086,8 @@ constexpr int FRING = 32;  // max ring slots (512 TMEM columns / HB)
 // in TMEM holds the running column PREFIX C of the R plane (as in the fused
 // kernel), so every output band is C(y+p) - C(y-p-1) windows with no running
 // state and CG output warp groups emit bands j = g (mod CG) concurrently.
-//  * loader warps (4, one per TMEM lane quadrant): plane rows arrive through a
-//    cp.async ring tl.pf bands ahead; the loader accumulates C and appends each
+//  * loader warps (4, one per TMEM lane quadrant): plane bands arrive as TMA
+//    tensor loads (16 x 128 int32 boxes) tl.pf bands ahead; the loader accumulates C and appends each
 //    band to the ring after every output band that reads the overwritten band
 //    from TMEM is done (lag tl.lag = span + CG - 1 bands);
 //  * trails older than the ring (C5's largest boxes) are read from a shared-memory
@@ -1089,14 +1099,15 @@ constexpr int FRING = 32;  // max ring slots (512 TMEM columns / HB)
 constexpr int CG = 3;                          // output warp groups
 constexpr int C2THREADS = 32 * 4 * (1 + CG);   // loader group + CG output groups
 constexpr int C2DONE = 32;  // output-band done barriers: >= lag - span + 1, so no barrier is lapped
+constexpr int C2PF = 8;     // max plane-band slots (TMA ring)
 
 template <int K>
 __global__ void __launch_bounds__(C2THREADS, 1)
     cols2_kernel(const int* __restrict__ mid_in, float* __restrict__ dst, Geometry g, Taps t, Tiling tl,
-                 const __grid_constant__ CUtensorMap omap) {
+                 const __grid_constant__ CUtensorMap omap, const __grid_constant__ CUtensorMap mmap) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
-  __shared__ __align__(8) uint64_t full[FRING], done[C2DONE];
+  __shared__ __align__(8) uint64_t full[FRING], done[C2DONE], lfull[C2PF], lempty[C2PF];
   const int ch = blockIdx.x % g.in_px;
   const int sidx = blockIdx.x / g.in_px;
   const int strip = sidx % tl.nstrips;
@@ -1111,12 +1122,17 @@ __global__ void __launch_bounds__(C2THREADS, 1)
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const int D = tl.D, NB = D / HB, PF = tl.pf, DS = tl.ds;
-  int* lring = (int*)smem;                    // [PF][HB][WS] plane bands (cp.async)
+  unsigned char* abase = smem + (((smem_u32(smem) + 127u) & ~127u) - smem_u32(smem));  // TMA: 128-byte aligned
+  int* lring = (int*)abase;                   // [PF][HB][WS] plane bands (TMA tensor loads)
   int* dring = lring + PF * HB * WS;          // [DS][HB][WS] copies of old ring bands
-  float* obuf = (float*)(smem + (((smem_u32(smem) + tl.obuf_off + 127u) & ~127u) - smem_u32(smem)));
+  float* obuf = (float*)(abase + tl.obuf_off);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NB; ++i) mbar_init(&full[i], 32 * 4);
     for (int i = 0; i < C2DONE; ++i) mbar_init(&done[i], 32 * 4);
+    for (int i = 0; i < PF; ++i) {
+      mbar_init(&lfull[i], 1);   // the issuing thread's expect_tx + the TMA bytes
+      mbar_init(&lempty[i], 4);  // one arrive per loader warp
+    }
   }
   if (warp == 0) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
   tmem_fence_before();
@@ -1133,27 +1149,26 @@ __global__ void __launch_bounds__(C2THREADS, 1)
     uint32_t onum = 0;
     int oob = 0;     // next output band to observe: index onum, band oob of segment so
     int slot = 0;
+    // plane bands arrive by TMA (one 16 x 128 box per band, issued PF-1 bands ahead by
+    // thread 0) into PF slots with full (tx bytes) / empty (one arrive per warp) barriers
+    int lslot = 0, islot = 0;
+    uint32_t lph = 0, iph = 0;
+    int cslot = tl.copy_e % NB, dslot = 0;  // ring slot (v + copy_e) % NB and copy slot of the next band copy
     for (; sc.valid; sc.next()) {
       const int* mcol = mid_in + ch * g.mid_ch + (long long)sc.img * g.mid_img + xc;
       const long long mrow = g.mid_row;
       const int vstart = sc.a - 1 - t.pmax;
+      const int zc = ch * g.nimg + sc.img;
       auto issue = [&](int pb) {
-        if (pb < sc.nbands) {
-          int* sp = lring + (pb % PF) * (HB * WS) + c;
-          const int v0 = vstart + pb * HB;
-          if (v0 >= 0 && v0 + HB <= g.H) {
-            const int* gp = mcol + (long long)v0 * mrow;
-#pragma unroll
-            for (int r = 0; r < HB; ++r) {
-              cp_async4(sp + r * WS, gp);
-              gp += mrow;
-            }
-          } else {
-#pragma unroll
-            for (int r = 0; r < HB; ++r) cp_async4(sp + r * WS, mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
-          }
+        if (threadIdx.x == 0 && pb < sc.nbands) {
+          mbar_wait(&lempty[islot], iph ^ 1);
+          mbar_expect_tx(&lfull[islot], HB * WS * 4);
+          tma_load_3d(lring + islot * (HB * WS), &mmap, x0, vstart + pb * HB, zc, &lfull[islot]);
         }
-        cp_async_commit();
+        if (pb < sc.nbands && ++islot == PF) {
+          islot = 0;
+          iph ^= 1;
+        }
       };
       for (int pb = 0; pb < PF - 1; ++pb) issue(pb);
       int cprefix = 0;
@@ -1169,24 +1184,41 @@ __global__ void __launch_bounds__(C2THREADS, 1)
           }
         }
         if (DS > 0) {
-          // copy band u out of the ring before it is overwritten (see above)
-          const long long u = (long long)v - NB + tl.copy_e;
-          if (u >= 0) {
+          // copy band u = v - NB + copy_e out of the ring before it is overwritten (see above)
+          if ((long long)v >= (long long)NB - tl.copy_e) {
             uint32_t old[HB];
-            tmem_ld16(tlane + (uint32_t)((u % NB) * HB), old);
+            tmem_ld16(tlane + (uint32_t)(cslot * HB), old);
             tmem_wait_ld();
-            int* dp = dring + (int)(u % DS) * (HB * WS) + c;
+            int* dp = dring + dslot * (HB * WS) + c;
 #pragma unroll
             for (int r = 0; r < HB; ++r) dp[r * WS] = (int)old[r];
+            if (++dslot == DS) dslot = 0;
+          }
+          if (++cslot == NB) cslot = 0;
+        }
+        uint32_t cv[HB];
+        const int v0 = vstart + pb * HB;
+        mbar_wait(&lfull[lslot], lph);
+        if (v0 >= 0 && v0 + HB <= g.H) {
+          const int* lp = lring + lslot * (HB * WS) + c;
+#pragma unroll
+          for (int r = 0; r < HB; ++r) {
+            cprefix += lp[r * WS];
+            cv[r] = (uint32_t)cprefix;
+          }
+        } else {
+          // rows beyond the image edges replicate the border row (filtering.py:10-13)
+#pragma unroll
+          for (int r = 0; r < HB; ++r) {
+            cprefix += __ldg(mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
+            cv[r] = (uint32_t)cprefix;
           }
         }
-        cp_async_wait_depth(PF - 1);
-        const int* lp = lring + (pb % PF) * (HB * WS) + c;
-        uint32_t cv[HB];
-#pragma unroll
-        for (int r = 0; r < HB; ++r) {
-          cprefix += lp[r * WS];
-          cv[r] = (uint32_t)cprefix;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&lempty[lslot]);
+        if (++lslot == PF) {
+          lslot = 0;
+          lph ^= 1;
         }
         tmem_st16(tlane + (uint32_t)(slot * HB), cv);
         if (slot == 0) tmem_st16(tlane + (uint32_t)D, cv);  // mirror: lag windows never wrap
@@ -1195,7 +1227,6 @@ __global__ void __launch_bounds__(C2THREADS, 1)
         mbar_arrive(&full[slot]);
         if (++slot == NB) slot = 0;
       }
-      cp_async_wait_all();
     }
   } else {
     // ------------------------------------------------ output groups
