@@ -128,6 +128,22 @@ int sb_prefix_sum_f64(const double* src, double* dst, int64_t n, void* workspace
  * value_bound when the caller does not supply one. */
 int sb_max_abs(const void* src, int src_dtype, int64_t n, double* out_dev, void* stream);
 
+/* Sampled evaluation - replaces filtering.filter_at (filtering.py:107-148).
+ * out[n] = pixel (pt_y[n], cols[pt_col[n]]) of sb_separable_filter_2d of the
+ * (height, width) single-channel image `src` (bit-identical to it): the row
+ * pass runs only at the ncols touched columns `cols`, the column pass only at
+ * the npts points.  cols, pt_col, pt_y (int32) and out (npts floats) are device
+ * arrays; the caller guarantees 0 <= cols < width, 0 <= pt_col < ncols and
+ * 0 <= pt_y < height (the reference raises ValueError for points outside the
+ * image before any arithmetic).  Needs sb_filter_at_workspace_bytes(height,
+ * ncols) bytes of device workspace; value_bound and status_dev as in
+ * sb_separable_filter_2d. */
+size_t sb_filter_at_workspace_bytes(int64_t height, int64_t ncols);
+int sb_filter_at(const void* src, int src_dtype, int64_t height, int64_t width, int64_t src_row_stride,
+                 const int32_t* cols, int64_t ncols, const int32_t* pt_col, const int32_t* pt_y, int64_t npts,
+                 float* out, const int64_t* radii, const double* weights, int k, double value_bound, void* workspace,
+                 size_t workspace_bytes, int* status_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,8 @@ EXPORTED_SYMBOLS = (
     "sb_prefix_sum_workspace_bytes",
     "sb_prefix_sum_f64",
     "sb_max_abs",
+    "sb_filter_at_workspace_bytes",
+    "sb_filter_at",
 )
 
 
@@ -93,6 +95,11 @@ def _declare(lib):
     lib.sb_prefix_sum_f64.restype = _int
     lib.sb_max_abs.argtypes = [_vp, _int, _i64, _vp, _vp]
     lib.sb_max_abs.restype = _int
+    lib.sb_filter_at_workspace_bytes.argtypes = [_i64, _i64]
+    lib.sb_filter_at_workspace_bytes.restype = _size
+    lib.sb_filter_at.argtypes = [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64p, _f64p, _int,
+                                 ctypes.c_double, _vp, _size, _vp, _vp]
+    lib.sb_filter_at.restype = _int
 
 
 def load():

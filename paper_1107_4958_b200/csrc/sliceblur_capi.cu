@@ -408,7 +408,38 @@ int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, c
 
 extern "C" {
 
-int sb_version(void) { return 2; }
+int sb_version(void) { return 3; }
+
+size_t sb_filter_at_workspace_bytes(int64_t height, int64_t ncols) {
+  if (height < 1 || ncols < 1) return 0;
+  return (size_t)height * (size_t)ncols * sizeof(int);
+}
+
+int sb_filter_at(const void* src, int src_dtype, int64_t height, int64_t width, int64_t src_row_stride,
+                 const int32_t* cols, int64_t ncols, const int32_t* pt_col, const int32_t* pt_y, int64_t npts,
+                 float* out, const int64_t* radii, const double* weights, int k, double value_bound, void* workspace,
+                 size_t workspace_bytes, int* status_dev, void* stream) {
+  if (!src || !cols || !pt_col || !pt_y || !out || height < 1 || width < 1 || ncols < 1 || npts < 1)
+    return fail(SB_ERR_INVALID_ARGUMENT, "filter_at needs a non-empty image, columns and points");
+  if (src_row_stride < width) return fail(SB_ERR_INVALID_ARGUMENT, "row stride smaller than the width");
+  if (height > 0x7fffffffLL || width > 0x7fffffffLL || ncols > 65535)
+    return fail(SB_ERR_INVALID_ARGUMENT, "filter_at: image or column set too large");
+  int rc = sb_check_kernel(radii, weights, k, width);  // filtering.py:119-120
+  if (rc) return rc;
+  rc = sb_check_kernel(radii, weights, k, height);
+  if (rc) return rc;
+  Plan plan;
+  rc = make_taps(radii, weights, k, src_dtype, value_bound, &plan);
+  if (rc) return rc;
+  const size_t need = sb_filter_at_workspace_bytes(height, ncols);
+  if (!workspace || workspace_bytes < need)
+    return fail(SB_ERR_WORKSPACE, "workspace of " + std::to_string(need) + " bytes required");
+  const int e = sb::launch_filter_at(src, src_dtype, src_row_stride, (int)height, (int)width, cols, (int)ncols,
+                                     pt_col, pt_y, npts, out, (int*)workspace, plan.taps, status_dev,
+                                     (cudaStream_t)stream);
+  if (e) return cuda_fail((cudaError_t)e, "filter_at launch");
+  return SB_OK;
+}
 
 const char* sb_last_error(void) { return g_last_error.c_str(); }
 

@@ -1531,6 +1531,9 @@ const void* sweep_ptr_u8(Mode m, int k);
 const void* sweep_ptr_u16(Mode m, int k);
 const void* sweep_ptr_f32(Mode m, int k);
 const void* sweep_ptr_f64(Mode m, int k);
+int launch_filter_at(const void* src, int src_dtype, long long row_stride, int H, int W, const int* cols, int ncols,
+                     const int* pt_col, const int* pt_y, long long npts, float* out, int* R, const Taps& t, int* status,
+                     cudaStream_t st);  // filter_at.cu
 const void* sweep_ptr_cols(int k);   // ColsFromMid (source type unused)
 const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)

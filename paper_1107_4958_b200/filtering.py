@@ -29,6 +29,7 @@ from .approx import SliceKernel
 
 __all__ = [
     "KernelTooLargeError",
+    "filter_at",
     "separable_filter_window",
     "filter_rows",
     "prefix_sum",
@@ -390,3 +391,50 @@ def prefix_sum(values):
     _raise_for(lib.sb_prefix_sum_f64(t.data_ptr(), out.data_ptr(), n, workspace.data_ptr(), ws,
                                      torch.cuda.current_stream().cuda_stream))
     return out.cpu().numpy() if from_numpy else out
+
+
+def filter_at(image, kernel: SliceKernel, points, *, value_bound=None, check: bool = True):
+    """Evaluate the separable filter at selected (x, y) points only (filtering.py:107-148).
+
+    The row pass runs only at the touched columns and the column pass only at
+    the points (``sb_filter_at``); the values are bit-identical to the same
+    pixels of ``separable_filter_2d`` on the GPU, as the reference's are to its
+    own full filter.  Returns float32 values in point order (numpy for numpy
+    input, a CUDA tensor for CUDA tensor input).
+    """
+    if isinstance(image, np.ndarray) or not hasattr(image, "dim"):
+        if np.asarray(image).ndim != 2:
+            raise ValueError("need a 2D image")
+    elif image.dim() != 2:
+        raise ValueError("need a 2D image")
+    dev = _Device(image)
+    x = dev.tensor
+    h, w = x.shape
+    if min(h, w) < 1:
+        raise ValueError("need a non-empty 2D image")
+    _check_kernel(kernel, w)
+    _check_kernel(kernel, h)
+    pts = [(int(px), int(py)) for px, py in points]
+    for px, py in pts:
+        if not (0 <= px < w and 0 <= py < h):
+            raise ValueError(f"point ({px}, {py}) outside {w}x{h} image")
+    torch = dev.torch
+    if not pts:
+        empty = torch.empty(0, dtype=torch.float32, device=x.device)
+        return empty.cpu().numpy() if dev.from_numpy or dev.host_tensor else empty
+    cols = sorted({px for px, _ in pts})
+    index = {cx: i for i, cx in enumerate(cols)}
+    cols_d = torch.tensor(cols, dtype=torch.int32).to(x.device)
+    pt_col = torch.tensor([index[px] for px, _ in pts], dtype=torch.int32).to(x.device)
+    pt_y = torch.tensor([py for _, py in pts], dtype=torch.int32).to(x.device)
+    result = torch.empty(len(pts), dtype=torch.float32, device=x.device)
+    radii, weights, rp, wp = _kernel_arrays(kernel)
+    lib = nat.load()
+    ws_bytes = int(lib.sb_filter_at_workspace_bytes(h, len(cols)))
+    workspace = torch.empty(max(ws_bytes, 4), dtype=torch.uint8, device=x.device)
+    status = torch.zeros(1, dtype=torch.int32, device=x.device)
+    bound = dev.value_bound(value_bound)
+    _raise_for(lib.sb_filter_at(x.data_ptr(), dev.code, h, w, w, cols_d.data_ptr(), len(cols), pt_col.data_ptr(),
+                                pt_y.data_ptr(), len(pts), result.data_ptr(), rp, wp, kernel.k, bound,
+                                workspace.data_ptr(), ws_bytes, status.data_ptr(), dev.stream))
+    return dev.finish(result, status, check)

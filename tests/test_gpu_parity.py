@@ -327,3 +327,54 @@ def test_two_launch_path_configs(shape, k, sigma, ch, batch):
             res = got[bi, :, :, c] if ch > 1 else got[bi]
             err = np.abs(res - ref)
             assert err.max() <= BAR, (shape, k, sigma, ch, batch, float(err.max()))
+
+
+def test_filter_at_golden_and_bit_identical_to_full_filter(golden_cases):
+    # the reference's filter_at golden vector (filtering.py:107-148) within the bar,
+    # and bit-identical to the GPU's own full filter at the same pixels
+    z = golden_cases
+    img = z["filter_at/image"]
+    kern = A.SliceKernel(z["filter_at/radii"], z["filter_at/weights"])
+    pts = [tuple(int(v) for v in p) for p in z["filter_at/points"]]
+    got = F.filter_at(img, kern, pts)
+    assert got.shape == (len(pts),)
+    assert np.abs(got - z["filter_at/out"]).max() <= BAR
+    full = F.separable_filter_2d(img, kern)
+    np.testing.assert_array_equal(got, np.array([full[y, x] for x, y in pts], np.float32))
+
+
+@pytest.mark.parametrize("dtype,shape,k,sigma", [
+    (np.uint8, (300, 257), 3, 10.0),     # fused-path pixels (uint8 float2 prefixes)
+    (np.float32, (200, 180), 4, 32.0),   # fused, int32 prefixes
+    (np.float32, (700, 600), 4, 100.0),  # two-launch path (plane + prefix-form columns)
+    (np.uint16, (96, 130), 5, 8.0),
+])
+def test_filter_at_matches_full_filter_pixels(dtype, shape, k, sigma):
+    rng = np.random.default_rng(77)
+    h, w = shape
+    scale = 65535 if dtype == np.uint16 else 255
+    img = (rng.random(shape) * scale).astype(dtype)
+    kern = A.table_kernel(k, sigma)
+    # corners, edges, repeated columns, repeated points, arbitrary order
+    pts = [(0, 0), (w - 1, h - 1), (0, h - 1), (w - 1, 0), (w // 2, h // 2), (w // 2, 3), (w // 2, 3), (5, h - 2)]
+    pts += [(int(rng.integers(w)), int(rng.integers(h))) for _ in range(40)]
+    bound = None if dtype in (np.uint8, np.uint16) else float(scale)
+    got = F.filter_at(img, kern, pts, value_bound=bound)
+    full = F.separable_filter_2d(img, kern, value_bound=bound)
+    np.testing.assert_array_equal(got, np.array([full[y, x] for x, y in pts], np.float32))
+    ref = O.filter_at(np.asarray(img, np.float64), kern.radii, kern.weights, pts)
+    assert np.abs(got - ref).max() <= BAR * scale / 255.0
+
+
+def test_filter_at_errors_mirror_reference():
+    img = np.zeros((32, 32), np.float32)
+    kern = A.table_kernel(3, 1.0)
+    with pytest.raises(ValueError, match="outside"):
+        F.filter_at(img, kern, [(16, 32)])
+    with pytest.raises(ValueError, match="outside"):
+        F.filter_at(img, kern, [(0, -1)])
+    with pytest.raises(ValueError):
+        F.filter_at(np.zeros(5), kern, [(0, 0)])
+    with pytest.raises(F.KernelTooLargeError):
+        F.filter_at(np.zeros((4, 40)), A.table_kernel(3, 3.0), [(1, 1)])
+    assert F.filter_at(img, kern, []).shape == (0,)

@@ -37,7 +37,7 @@ def test_exports_every_header_symbol(lib):
     assert set(syms) == set(nat.EXPORTED_SYMBOLS)
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.sb_version() == 2
+    assert lib.sb_version() == 3
 
 
 def _k(radii, weights):
@@ -84,6 +84,16 @@ def test_invalid_arguments_fail_before_cuda(lib):
         nat.SB_ERR_INVALID_ARGUMENT
     assert lib.sb_slice_filter_1d(1, nat.SB_DTYPE_F32, 0, 1, rp, wp, 3, 1.0, None, None) == nat.SB_ERR_INVALID_ARGUMENT
     assert lib.sb_prefix_sum_f64(None, None, 0, None, 0, None) == nat.SB_ERR_INVALID_ARGUMENT
+    # filter_at: empty point set / NULL arrays / kernel larger than the image
+    fa = lib.sb_filter_at
+    assert fa(1, nat.SB_DTYPE_F32, 64, 64, 64, 1, 1, 1, 1, 0, 1, rp, wp, 3, 255.0, None, 0, None, None) == \
+        nat.SB_ERR_INVALID_ARGUMENT
+    assert fa(1, nat.SB_DTYPE_F32, 64, 64, 64, None, 1, 1, 1, 1, 1, rp, wp, 3, 255.0, None, 0, None, None) == \
+        nat.SB_ERR_INVALID_ARGUMENT
+    assert fa(1, nat.SB_DTYPE_F32, 64, 11, 64, 1, 1, 1, 1, 1, 1, rp, wp, 3, 255.0, None, 0, None, None) == \
+        nat.SB_ERR_KERNEL_TOO_LARGE
+    assert fa(1, nat.SB_DTYPE_F32, 64, 64, 64, 1, 1, 1, 1, 1, 1, rp, wp, 3, 255.0, None, 0, None, None) == \
+        nat.SB_ERR_WORKSPACE
 
 
 def test_workspace_sizes(lib):
@@ -94,4 +104,5 @@ def test_workspace_sizes(lib):
     r, w, rp, wp = _k(big.radii, big.weights)
     assert lib.sb_separable_filter_2d_workspace_bytes(nat.SB_DTYPE_F32, 1, 1000, 2000, 3, rp, 4) == 1000 * 2000 * 3 * 4
     assert lib.sb_prefix_sum_workspace_bytes(1) == 8
+    assert lib.sb_filter_at_workspace_bytes(1000, 3) == 1000 * 3 * 4
     assert lib.sb_prefix_sum_workspace_bytes(2048 * 3 + 1) == 4 * 8
