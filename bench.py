@@ -349,6 +349,17 @@ def run_ours(args, cfg):
             diff = got[:, cols].astype(np.float64) - ref
         max_abs = float(np.abs(diff).max())
         rmse = float(np.sqrt(np.mean(diff * diff)))
+    # quality of the K-box approximation against the dense truncated Gaussian (the
+    # reference's own harness, oracle.py:58-102, here on the GPU), image 0, [0, 1] scale
+    quality = None
+    if not strips and cfg["h"] * cfg["w"] <= 8192 * 8192:
+        from paper_1107_4958_b200 import quality as Q
+
+        img0 = x[0] if not channels_last else x[0][:, :, 0].contiguous()
+        fast0 = out[0] if not channels_last else out[0][:, :, 0].contiguous()
+        exact0 = Q.exact_gaussian_2d(img0, cfg["sigma"])
+        quality = {"psnr_db_vs_exact_gaussian": round(Q.psnr(fast0 / 255.0, exact0 / 255.0), 3),
+                   "scope": "rank-0 image 0 (channel 0), values / 255, exact = dense Gaussian r = ceil(pi*sigma)"}
 
     if world > 1:
         dist.barrier()
@@ -381,11 +392,12 @@ def run_ours(args, cfg):
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes_per_step": alg_bytes,
                      "kernel": "fused_kernel (one launch per step)" if ws == 0 else
-                               "stream_rows_kernel + cols_kernel (two launches per step, timed together)"},
+                               "stream_rows_kernel + cols2_kernel (two launches per step, timed together)"},
         "e2e": {"value": round(e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(in_bytes),
                 "d2h_bytes_per_step": int(out_bytes)},
         "gpu_launches": int(args.steps * launches_per_step),
         "parity": {"max_abs": max_abs, "rmse": rmse, "scope": "rank-0 image 0 vs C oracle"},
+        "quality": quality,
         "clocks": clocks,
     }
     if cpu:

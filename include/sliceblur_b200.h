@@ -128,6 +128,21 @@ int sb_prefix_sum_f64(const double* src, double* dst, int64_t n, void* workspace
  * value_bound when the caller does not supply one. */
 int sb_max_abs(const void* src, int src_dtype, int64_t n, double* out_dev, void* stream);
 
+/* Accuracy harness - replaces oracle.exact_gaussian_2d and the sum behind
+ * oracle.mse / oracle.psnr (reference oracle.py:58-102).  Not the hot path.
+ * sb_exact_gaussian_2d: dense separable correlation with the ntaps (odd) fp64
+ * taps in taps_dev (gaussian_taps(sigma): truncation radius ceil(pi*sigma),
+ * sum 1), replicate boundary, rows then columns, fp64 (height, width) output in
+ * dst; bit-identical to the reference's numpy arithmetic.  Needs
+ * sb_exact_gaussian_workspace_bytes(height, width) bytes of workspace.
+ * sb_sum_sq_diff: *out_dev += sum (a[i] - b[i])^2 in fp64 over n elements
+ * (a, b: SB_DTYPE_F32 or SB_DTYPE_F64 device arrays). */
+size_t sb_exact_gaussian_workspace_bytes(int64_t height, int64_t width);
+int sb_exact_gaussian_2d(const void* src, int src_dtype, int64_t height, int64_t width, int64_t src_row_stride,
+                         const double* taps_dev, int ntaps, double* dst, void* workspace, size_t workspace_bytes,
+                         void* stream);
+int sb_sum_sq_diff(const void* a, int a_dtype, const void* b, int b_dtype, int64_t n, double* out_dev, void* stream);
+
 /* Sampled evaluation - replaces filtering.filter_at (filtering.py:107-148).
  * out[n] = pixel (pt_y[n], cols[pt_col[n]]) of sb_separable_filter_2d of the
  * (height, width) single-channel image `src` (bit-identical to it): the row

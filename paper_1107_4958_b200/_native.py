@@ -43,6 +43,9 @@ EXPORTED_SYMBOLS = (
     "sb_max_abs",
     "sb_filter_at_workspace_bytes",
     "sb_filter_at",
+    "sb_exact_gaussian_workspace_bytes",
+    "sb_exact_gaussian_2d",
+    "sb_sum_sq_diff",
 )
 
 
@@ -100,6 +103,12 @@ def _declare(lib):
     lib.sb_filter_at.argtypes = [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64p, _f64p, _int,
                                  ctypes.c_double, _vp, _size, _vp, _vp]
     lib.sb_filter_at.restype = _int
+    lib.sb_exact_gaussian_workspace_bytes.argtypes = [_i64, _i64]
+    lib.sb_exact_gaussian_workspace_bytes.restype = _size
+    lib.sb_exact_gaussian_2d.argtypes = [_vp, _int, _i64, _i64, _i64, _vp, _int, _vp, _vp, _size, _vp]
+    lib.sb_exact_gaussian_2d.restype = _int
+    lib.sb_sum_sq_diff.argtypes = [_vp, _int, _vp, _int, _i64, _vp, _vp]
+    lib.sb_sum_sq_diff.restype = _int
 
 
 def load():

@@ -179,8 +179,37 @@ def filter_cases(sb):
     return cases
 
 
+def quality_cases(sb):
+    """The reference's accuracy harness (oracle.py:58-102): dense truncated Gaussian
+    taps, ``exact_gaussian_2d``, and ``mse`` / ``psnr`` of the running-sum filter
+    against it, on small seeded images."""
+    import sliceblur.oracle as so  # noqa: E402
+
+    rng = np.random.default_rng(20261)
+    cases = {}
+    for name, shape, sigma, k in [("q40x50_s1p5", (40, 50), 1.5, 3), ("q64x80_s3", (64, 80), 3.0, 4),
+                                  ("q120x96_s8", (120, 96), 8.0, 5)]:
+        img = rng.random(shape)
+        kern = sb.table_kernel(k, sigma) if hasattr(sb, "table_kernel") else None
+        if kern is None:
+            from sliceblur.approx import scale_to_sigma, table_defaults, to_slices
+            kern = scale_to_sigma(to_slices(*table_defaults(k)), sigma)
+        exact = so.exact_gaussian_2d(img, sigma)
+        fast = sb.separable_filter_2d(img, kern)
+        cases[name + "/image"] = img
+        cases[name + "/sigma"] = np.float64(sigma)
+        cases[name + "/taps"] = so.gaussian_taps(sigma)
+        cases[name + "/exact"] = exact
+        cases[name + "/radii"] = kern.radii
+        cases[name + "/weights"] = kern.weights
+        cases[name + "/mse"] = np.float64(so.mse(fast, exact))
+        cases[name + "/psnr"] = np.float64(so.psnr(fast, exact))
+    return cases
+
+
 def main():
     sb = _load_reference()
+    np.savez_compressed(os.path.join(HERE, "quality_cases.npz"), **quality_cases(sb))
     params = box_params(sb)
     with open(os.path.join(HERE, "box_params.json"), "w") as fh:
         json.dump(params, fh, indent=1, sort_keys=True)

@@ -378,3 +378,27 @@ def test_filter_at_errors_mirror_reference():
     with pytest.raises(F.KernelTooLargeError):
         F.filter_at(np.zeros((4, 40)), A.table_kernel(3, 3.0), [(1, 1)])
     assert F.filter_at(img, kern, []).shape == (0,)
+
+
+def test_quality_harness_matches_reference():
+    # the reference's exact_gaussian_2d / mse / psnr (oracle.py:58-102) on its own
+    # golden vectors: the dense Gaussian is bit-identical, the metrics within 1e-9
+    from paper_1107_4958_b200 import quality as Q
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "quality_cases.npz"))
+    for name in sorted({k.split("/")[0] for k in z.files}):
+        img, sigma = z[name + "/image"], float(z[name + "/sigma"])
+        np.testing.assert_array_equal(Q.gaussian_taps(sigma), z[name + "/taps"])
+        exact = Q.exact_gaussian_2d(img, sigma)
+        np.testing.assert_array_equal(exact, z[name + "/exact"])
+        kern = A.SliceKernel(z[name + "/radii"], z[name + "/weights"])
+        fast = F.separable_filter_2d(img, kern, value_bound=1.0)
+        # the fast path is float32 within the bar; the metric itself is exact on its inputs
+        ref_mse = float(np.mean((np.asarray(fast, np.float64) - exact) ** 2))
+        assert Q.mse(fast, exact) == pytest.approx(ref_mse, rel=1e-9)
+        assert Q.psnr(fast, exact) == pytest.approx(float(z[name + "/psnr"]), abs=0.05)
+    assert Q.psnr(np.ones((4, 4)), np.ones((4, 4))) == Q.PSNR_INF
+    with pytest.raises(ValueError):
+        Q.mse(np.zeros((2, 3)), np.zeros((3, 2)))
+    with pytest.raises(ValueError):
+        Q.gaussian_taps(0.0)
