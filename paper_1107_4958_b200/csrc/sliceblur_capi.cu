@@ -230,7 +230,7 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
   if (slack < 0) slack = 3;
   for (; slack >= 0; --slack) {
     tl.lag = span + sb::CG - 1 + slack;
-    tl.copy_e = tl.lag - span;
+    tl.copy_e = tl.lag - span + 1;  // band v - NB + copy_e is copied right after band v is released
     // output band o + C2DONE may finish before the loader observed band o's done phase
     // unless the loader has passed o by then: C2DONE >= lag - span + 1
     if (tl.lag - span + 1 > sb::C2DONE) continue;
@@ -245,7 +245,7 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
       if ((pmax + 1 + (int)radii[i]) / sb::HB <= thr) ok = false;   // leads always from the ring
     }
     if (!ok) continue;
-    tl.ds = thr >= 0 ? 2 * tl.lag - NB - span + 1 : 0;
+    tl.ds = thr >= 0 ? 2 * tl.lag - NB - span + 2 : 0;  // >= lag - NB + copy_e, plus one spare
     tl.pf = 0;
     for (int pf : {sb::C2PF, 6, 4, 3, 2})
       if ((size_t)(pf + tl.ds) * band + obuf <= kSmemBudget) {

@@ -1183,29 +1183,24 @@ __global__ void __launch_bounds__(C2THREADS, 1)
             oob = 0;
           }
         }
-        if (DS > 0) {
-          // copy band u = v - NB + copy_e out of the ring before it is overwritten (see above)
-          if ((long long)v >= (long long)NB - tl.copy_e) {
-            uint32_t old[HB];
-            tmem_ld16(tlane + (uint32_t)(cslot * HB), old);
-            tmem_wait_ld();
-            int* dp = dring + dslot * (HB * WS) + c;
-#pragma unroll
-            for (int r = 0; r < HB; ++r) dp[r * WS] = (int)old[r];
-            if (++dslot == DS) dslot = 0;
-          }
-          if (++cslot == NB) cslot = 0;
-        }
         uint32_t cv[HB];
         const int v0 = vstart + pb * HB;
         mbar_wait(&lfull[lslot], lph);
         if (v0 >= 0 && v0 + HB <= g.H) {
           const int* lp = lring + lslot * (HB * WS) + c;
+          int e[HB];
 #pragma unroll
-          for (int r = 0; r < HB; ++r) {
-            cprefix += lp[r * WS];
-            cv[r] = (uint32_t)cprefix;
+          for (int r = 0; r < HB; ++r) e[r] = lp[r * WS];
+          // running prefix with a two-element stride: odd entries chain by 3-input adds,
+          // even entries hang off them (dependency depth 9 instead of 16)
+          int odd = cprefix;
+#pragma unroll
+          for (int r = 0; r < HB; r += 2) {
+            cv[r] = (uint32_t)(odd + e[r]);
+            odd = odd + e[r] + e[r + 1];
+            cv[r + 1] = (uint32_t)odd;
           }
+          cprefix = odd;
         } else {
           // rows beyond the image edges replicate the border row (filtering.py:10-13)
 #pragma unroll
@@ -1226,6 +1221,20 @@ __global__ void __launch_bounds__(C2THREADS, 1)
         tmem_fence_before();
         mbar_arrive(&full[slot]);
         if (++slot == NB) slot = 0;
+        if (DS > 0) {
+          // after releasing band v: copy band u = v - NB + copy_e out of the ring (its
+          // readers wait for band v + 1 or later; see cols_prefix_tiling)
+          if ((long long)v >= (long long)NB - tl.copy_e) {
+            uint32_t old[HB];
+            tmem_ld16(tlane + (uint32_t)(cslot * HB), old);
+            tmem_wait_ld();
+            int* dp = dring + dslot * (HB * WS) + c;
+#pragma unroll
+            for (int r = 0; r < HB; ++r) dp[r * WS] = (int)old[r];
+            if (++dslot == DS) dslot = 0;
+          }
+          if (++cslot == NB) cslot = 0;
+        }
       }
     }
   } else {
