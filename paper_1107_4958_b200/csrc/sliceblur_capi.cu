@@ -507,7 +507,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
   g.aligned16 = ((uintptr_t)src % 16 == 0) && ((src_row_stride * g.es) % 16 == 0) &&
                 (batch == 1 || (src_image_stride * g.es) % 16 == 0);
   g.out_bulk = channels == 1 && ((uintptr_t)dst % 16 == 0) && ((dst_row_stride * 4) % 16 == 0) &&
-               (batch == 1 || (dst_image_stride * 4) % 16 == 0) && getenv("SB_NO_TMA_STORE") == nullptr;
+               (batch == 1 || (dst_image_stride * 4) % 16 == 0);
   const long long total_rows = (long long)batch * (row_end - row_begin);  // rows the column sweep outputs
   const long long all_rows = (long long)batch * height;                   // rows the row pass produces
   const bool u8_single = (src_dtype == SB_DTYPE_U8 && channels == 1);

@@ -487,22 +487,35 @@ __device__ __forceinline__ void band_rows_f2(const float2* __restrict__ P, int c
 // column PREFIX C of the rounded row values (exact int32, wraps): the box sum of
 // slice i at row y is C(y+p_i) - C(y-p_i-1), a difference of two 16-row windows
 // (contiguous thanks to the mirrored first band), with no running state.
+#ifndef SB_COL_GROUP
+#define SB_COL_GROUP 2
+#endif
 template <int K>
 __device__ __forceinline__ void column_band_tmem(uint32_t tlane, const int (&lead_s)[K], const int (&trail_s)[K],
                                                  const Taps& t, float (&out)[HB]) {
   float2 o2[HB / 2];
+  // boxes in pairs: four window loads in flight per tcgen05.wait (latency, not bandwidth, bounds this)
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    uint32_t lv[HB], tv[HB];
-    tmem_ld16(tlane + (uint32_t)lead_s[i], lv);
-    tmem_ld16(tlane + (uint32_t)trail_s[i], tv);
+  for (int i0 = 0; i0 < K; i0 += SB_COL_GROUP) {
+    uint32_t lv[SB_COL_GROUP][HB], tv[SB_COL_GROUP][HB];
+#pragma unroll
+    for (int d = 0; d < SB_COL_GROUP; ++d)
+      if (i0 + d < K) {
+        tmem_ld16(tlane + (uint32_t)lead_s[i0 + d], lv[d]);
+        tmem_ld16(tlane + (uint32_t)trail_s[i0 + d], tv[d]);
+      }
     tmem_wait_ld();
-    const float2 w2 = make_float2(t.w_col[i], t.w_col[i]);
 #pragma unroll
-    for (int r = 0; r < HB / 2; ++r) {
-      // exact box sums of rows 2r, 2r+1, weighted with one packed FFMA2
-      const float2 d = make_float2(i2f_fast(lv[2 * r] - tv[2 * r]), i2f_fast(lv[2 * r + 1] - tv[2 * r + 1]));
-      o2[r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, o2[r]);
+    for (int d = 0; d < SB_COL_GROUP; ++d) {
+      const int i = i0 + d;
+      if (i >= K) break;
+      const float2 w2 = make_float2(t.w_col[i], t.w_col[i]);
+#pragma unroll
+      for (int r = 0; r < HB / 2; ++r) {
+        // exact box sums of rows 2r, 2r+1, weighted with one packed FFMA2
+        const float2 dd = make_float2(i2f_fast(lv[d][2 * r] - tv[d][2 * r]), i2f_fast(lv[d][2 * r + 1] - tv[d][2 * r + 1]));
+        o2[r] = i == 0 ? __fmul2_rn(w2, dd) : __ffma2_rn(w2, dd, o2[r]);
+      }
     }
   }
 #pragma unroll
@@ -924,12 +937,10 @@ __global__ void __launch_bounds__(FTHREADS, 2)
         const int pbi = pw * tl.npb + (int)(kb & (uint32_t)(tl.npb - 1));  // npb is 1 or 2
         int* P = Pbase + pbi * pbuf_words;
         mbar_wait_sleep(&bar_empty[pbi], ((kb >> (tl.npb - 1)) & 1) ^ 1);  // consumers done with it
-#ifndef SB_EXP_NOSCAN
         if (packed)
           scan_rows_b2_dispatch(cur, (float2*)P, tl);
         else
           scan_rows<Tin>(cur, P, g, t, tl, ch, n, status, 0, 1);
-#endif
         mbar_arrive(&bar_full[pbi]);
       }
       gb0 += (uint32_t)nbands;
@@ -998,12 +1009,7 @@ __global__ void __launch_bounds__(FTHREADS, 2)
             trail_s[i] = tr >= D ? tr - D : tr;
           }
           float ov[HB];
-#ifndef SB_EXP_NOCOL
           column_band_tmem<K>(tlane, lead_s, trail_s, t, ov);
-#else
-#pragma unroll
-          for (int r = 0; r < HB; ++r) ov[r] = (float)lead_s[r % K];
-#endif
           if (g.out_bulk && nb == HB) {
             // stage the band (row r of this warp's 32 columns at ob[r][lane]) and let one
             // TMA tensor store write the 16 x 32 box: no per-row address arithmetic
