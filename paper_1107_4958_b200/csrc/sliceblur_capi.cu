@@ -533,7 +533,8 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
   const int lagc = (sb::CW - 1 - xs + plan.pmax) / sb::CW;
   if (src_dtype == SB_DTYPE_F32 && lagc + 1 < sb::NSLOT) {
     const void* fs = sb::sweep_ptr_stream_f32(k);
-    const size_t smem = (size_t)sb::NPROD * 2 * 8 * sb::CW * sizeof(float) + (size_t)sb::HB * sb::RL * sizeof(int);
+    const size_t smem = (size_t)sb::NPROD * 2 * 8 * (sb::CW * sizeof(float) + sb::SRB_PAD) +
+                        (size_t)sb::HB * sb::RLS * sizeof(int);
     cudaError_t e = cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     int dev = 0, sms = 148;

@@ -1368,6 +1368,8 @@ constexpr int CW = 128;    // chunk width (= consumer threads)
 constexpr int RL = 1024;   // prefix ring length (power of two, >= 3*CW + 2*pmax + 2)
 
 constexpr int NSLOT = RL / CW;  // ring chunk slots; one full/done mbarrier per slot (no phase aliasing)
+constexpr int RLS = RL + 4;     // prefix ring row stride in words: 4112 B = 16 (mod 128)
+constexpr int SRB_PAD = 16;     // staged rows are CW*4 + 16 bytes apart: 16 (mod 128)
 
 template <typename Tin, int K>
 __global__ void __launch_bounds__(FUSED_THREADS, 2)
@@ -1375,7 +1377,6 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
                        int nbands_total, int* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
-  __shared__ int carry_s[HB];
   const int warp = threadIdx.x >> 5;
   const bool producer = warp >= NCONS;
   const int qtotal = g.W - xs + t.pmax;  // virtual columns q = x - xs, x in [xs, W + pmax)
@@ -1383,9 +1384,11 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
   const int nout = (g.W + CW - 1) / CW;
   // output chunk o reads prefix columns of input chunks o .. o + lagc
   const int lagc = (CW - 1 - xs + t.pmax) / CW;
-  const int rowbytes = CW * (int)sizeof(Tin);
-  unsigned char* stage = smem;                           // [NPROD][2][8][CW] elements
-  int* P = (int*)(smem + NPROD * 2 * 8 * rowbytes);      // [HB][RL]
+  // staged rows and prefix-ring rows are an odd multiple of 16 bytes apart, so the 8 lanes
+  // of a 128-bit access phase (8 rows, same chunk) hit 8 distinct bank groups
+  const int rowbytes = CW * (int)sizeof(Tin) + SRB_PAD;
+  unsigned char* stage = smem;                           // [NPROD][2][8][rowbytes]
+  int* P = (int*)(smem + NPROD * 2 * 8 * rowbytes);      // [HB][RLS]
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSLOT; ++i) {
@@ -1440,8 +1443,9 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
         }
         cp_async_commit();
       };
-      if (lane < 8) carry_s[8 * pw + lane] = 0;
-      __syncwarp();
+      // lane -> row rr = lane & 7 of this warp's 8 and chunk (lane >> 3) + 4*pass of the 8
+      // CH-column chunks; the row's running prefix (carry) lives in the 4 lanes of that row
+      int carry = 0;
       issue(0, 0);
       bool bad = false;
       for (int j = 0; j < nin; ++j) {
@@ -1456,7 +1460,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
         const unsigned char* cur = mystage + (j & 1) * 8 * rowbytes;
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
-          const int rr = pass * 4 + (lane >> 3), sc = lane & 7;
+          const int rr = lane & 7, sc = (lane >> 3) + 4 * pass;
           const Tin* e = (const Tin*)(cur + rr * rowbytes) + sc * CH;
           int v[CH];
           int tot = 0;
@@ -1465,23 +1469,18 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
             tot += to_fixed<Tin>(e[m], t, bad);
             v[m] = tot;
           }
+          // inclusive scan of the chunk totals over the row's 4 lanes (rr, rr+8, rr+16, rr+24)
           int inc = tot;
-#pragma unroll
-          for (int o = 1; o < 8; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, inc, o, 8);
-            if (sc >= o) inc += y;
-          }
-          const int r = 8 * pw + rr;
-          const int cin = carry_s[r];
-          const int off = cin + inc - tot;
-          int* dst = P + r * RL + ((j * CW + sc * CH) & (RL - 1));
+          int y = __shfl_up_sync(0xffffffffu, inc, 8);
+          if (lane >= 8) inc += y;
+          y = __shfl_up_sync(0xffffffffu, inc, 16);
+          if (lane >= 16) inc += y;
+          const int off = carry + inc - tot;
+          int* dst = P + (8 * pw + rr) * RLS + ((j * CW + sc * CH) & (RL - 1));
 #pragma unroll
           for (int m = 0; m < CH / 4; ++m)
             ((int4*)dst)[m] = make_int4(v[4 * m] + off, v[4 * m + 1] + off, v[4 * m + 2] + off, v[4 * m + 3] + off);
-          const int total_row = __shfl_sync(0xffffffffu, inc, 7, 8);
-          __syncwarp();
-          if (sc == 0) carry_s[r] = cin + total_row;
-          __syncwarp();
+          carry += __shfl_sync(0xffffffffu, inc, rr + 24);  // the row's total over these 4 chunks
         }
         mbar_arrive(&bar_full[gj % NSLOT]);
       }
@@ -1508,7 +1507,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
           const int* pt = P + ((x - xs - t.p[i] - 1) & (RL - 1));
           const float wi = t.w_row[i];
 #pragma unroll
-          for (int r = 0; r < HB; ++r) rv[r] = fmaf(wi, (float)(pl[r * RL] - pt[r * RL]), rv[r]);
+          for (int r = 0; r < HB; ++r) rv[r] = fmaf(wi, (float)(pl[r * RLS] - pt[r * RLS]), rv[r]);
         }
         const uint32_t go = out_ctr + o;
         mbar_arrive(&bar_done[go % NSLOT]);
