@@ -1498,23 +1498,28 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
         const uint32_t gj = cin_ctr + min(o + lagc, nin - 1);  // chunks complete in order
         mbar_wait(&bar_full[gj % NSLOT], (gj / NSLOT) & 1);
         const int x = o * CW + c;
-        float rv[HB];
-#pragma unroll
-        for (int r = 0; r < HB; ++r) rv[r] = 0.0f;
+        float2 rv[HB / 2];  // rows (2r, 2r+1): packed FMUL2 / FFMA2 / FADD2
 #pragma unroll
         for (int i = 0; i < K; ++i) {
           const int* pl = P + ((x - xs + t.p[i]) & (RL - 1));
           const int* pt = P + ((x - xs - t.p[i] - 1) & (RL - 1));
-          const float wi = t.w_row[i];
+          const float2 w2 = make_float2(t.w_row[i], t.w_row[i]);
 #pragma unroll
-          for (int r = 0; r < HB; ++r) rv[r] = fmaf(wi, (float)(pl[r * RLS] - pt[r * RLS]), rv[r]);
+          for (int r = 0; r < HB / 2; ++r) {
+            const float2 d = make_float2(i2f_fast((uint32_t)(pl[2 * r * RLS] - pt[2 * r * RLS])),
+                                         i2f_fast((uint32_t)(pl[(2 * r + 1) * RLS] - pt[(2 * r + 1) * RLS])));
+            rv[r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, rv[r]);
+          }
         }
         const uint32_t go = out_ctr + o;
         mbar_arrive(&bar_done[go % NSLOT]);
         if (x < g.W) {
 #pragma unroll
-          for (int r = 0; r < HB; ++r)
-            if (r < nrows) midrow[r][x] = __float_as_int(rv[r] + kMagic) - kMagicBits;
+          for (int r = 0; r < HB / 2; ++r) {
+            const float2 q = __fadd2_rn(rv[r], make_float2(kMagic, kMagic));  // round to the mid quantum
+            if (2 * r < nrows) midrow[2 * r][x] = __float_as_int(q.x) - kMagicBits;
+            if (2 * r + 1 < nrows) midrow[2 * r + 1][x] = __float_as_int(q.y) - kMagicBits;
+          }
         }
       }
     }
