@@ -147,6 +147,7 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
   while (lpr < nchunk && lpr < 32) lpr <<= 1;
   tl.lanes_per_row = lpr;
   tl.stage_row_bytes = ceil16(tl.L * staged_ch * es);
+  if (m == sb::Mode::Fused && (tl.stage_row_bytes / 16) % 2 == 0) tl.stage_row_bytes += 16;  // odd x 16 B: no conflicts
   tl.ls = (m == sb::Mode::Fused) ? sb::LS : tl.L;
   tl.packed = (m == sb::Mode::Fused && u8_single && ((tl.L + 63) & ~63) <= 192) ? 1 : 0;  // float2 prefixes
   if (tl.packed) {
@@ -196,7 +197,7 @@ size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
 
 bool fused_fits(int pmax, int channels, int es) {
   sb::Tiling tl = make_tiling(sb::Mode::Fused, pmax, channels, es, false);
-  return tl.L <= sb::LS && tl.tmem_cols <= 512 && smem_bytes(tl, sb::Mode::Fused) <= kSmemBudget;
+  return tl.L <= sb::LMAX && tl.tmem_cols <= 512 && smem_bytes(tl, sb::Mode::Fused) <= kSmemBudget;
 }
 
 const void* pick_kernel(sb::Mode m, int dtype, int k) {

@@ -46,7 +46,8 @@ constexpr int HB = 16;          // rows per band
 constexpr int WS = 128;         // strip width = threads per CTA
 constexpr int NWARPS = WS / 32;
 constexpr int CH = 16;          // px per scan chunk (one lane)
-constexpr int LS = 512;         // prefix row stride in words (compile-time: immediate offsets)
+constexpr int LS = 516;         // fused prefix row stride in words (compile-time offsets; 2064 B = 16 mod 128)
+constexpr int LMAX = 512;       // longest staged / prefix row of the fused sweep
 constexpr int LSP2 = 194;       // uint8 float2-prefix row stride (L <= 192): 1552 B = 16 (mod 128), conflict-free
 constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + kMagic rounds x to an integer (|x| < 2^22)
 constexpr int kMagicBits = 0x4B400000;  // bits(kMagic + n) = kMagicBits + n
@@ -375,6 +376,66 @@ __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restr
           dst[m] = make_int4(v[4 * m] + carry, v[4 * m + 1] + carry, v[4 * m + 2] + carry, v[4 * m + 3] + carry);
       }
       running += __shfl_sync(0xffffffffu, inc, lpr - 1, lpr);
+    }
+  }
+  if (bad && status) atomicOr(status, SB_STATUS_RANGE);
+}
+
+// The same scan for one warp over a whole band, bank-conflict free: lane (rr, cq)
+// = (lane & 7, lane >> 3) takes chunk cg + cq of row r0 + rr, so each 8-lane
+// phase of the 128-bit staging loads and prefix stores touches 8 rows of one
+// chunk, which sit in 8 distinct bank groups (row strides are an odd multiple of
+// 16 bytes); the row prefix of the chunk groups already done is carried in the
+// row's 4 lanes.
+template <typename Tin>
+__device__ __forceinline__ void scan_band8(const unsigned char* buf, int* __restrict__ P, const Geometry& g,
+                                           const Taps& t, const Tiling& tl, int ch, int n, int* status) {
+  const int lane = threadIdx.x & 31;
+  const int rr = lane & 7, cq = lane >> 3;
+  const int nchunk = tl.L / CH;
+  bool bad = false;
+  for (int r0 = 0; r0 < n; r0 += 8) {
+    const int r = r0 + rr;
+    int running = 0;
+    for (int cg = 0; cg < nchunk; cg += 4) {
+      const int chunk = cg + cq;
+      const bool live = (r < n) && (chunk < nchunk);
+      int v[CH];
+      int tot = 0;
+      if (live) {
+        const unsigned char* row = buf + r * tl.stage_row_bytes;
+        if (g.in_px == 1 && sizeof(Tin) * CH % 16 == 0) {
+          const uint4* p4 = (const uint4*)(row + chunk * CH * sizeof(Tin));
+          Tin e[CH];
+#pragma unroll
+          for (int m = 0; m < (int)(sizeof(Tin) * CH / 16); ++m) *(uint4*)((unsigned char*)e + 16 * m) = p4[m];
+#pragma unroll
+          for (int m = 0; m < CH; ++m) {
+            tot += to_fixed<Tin>(e[m], t, bad);
+            v[m] = tot;
+          }
+        } else {
+          const Tin* e = (const Tin*)row;
+#pragma unroll
+          for (int m = 0; m < CH; ++m) {
+            tot += to_fixed<Tin>(e[(chunk * CH + m) * g.in_px + ch], t, bad);
+            v[m] = tot;
+          }
+        }
+      }
+      int inc = tot;
+      int y = __shfl_up_sync(0xffffffffu, inc, 8);
+      if (cq >= 1) inc += y;
+      y = __shfl_up_sync(0xffffffffu, inc, 16);
+      if (cq >= 2) inc += y;
+      const int carry = running + inc - tot;
+      if (live) {
+        int4* dst = (int4*)(P + r * LS + chunk * CH);
+#pragma unroll
+        for (int m = 0; m < CH / 4; ++m)
+          dst[m] = make_int4(v[4 * m] + carry, v[4 * m + 1] + carry, v[4 * m + 2] + carry, v[4 * m + 3] + carry);
+      }
+      running += __shfl_sync(0xffffffffu, inc, rr + 24);
     }
   }
   if (bad && status) atomicOr(status, SB_STATUS_RANGE);
@@ -940,7 +1001,14 @@ __global__ void __launch_bounds__(FTHREADS, 2)
         if (packed)
           scan_rows_b2_dispatch(cur, (float2*)P, tl);
         else
-          scan_rows<Tin>(cur, P, g, t, tl, ch, n, status, 0, 1);
+        {
+          // uint8 sources only reach this for interleaved channels / long rows; keeping
+          // the lane-per-chunk scan there leaves the uint8 kernel's (hot) code unchanged
+          if constexpr (sizeof(Tin) == 1)
+            scan_rows<Tin>(cur, P, g, t, tl, ch, n, status, 0, 1);
+          else
+            scan_band8<Tin>(cur, P, g, t, tl, ch, n, status);
+        }
         mbar_arrive(&bar_full[pbi]);
       }
       gb0 += (uint32_t)nbands;
