@@ -248,13 +248,13 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
     if (!ok) continue;
     tl.ds = thr >= 0 ? 2 * tl.lag - NB - span + 2 : 0;  // >= lag - NB + copy_e, plus one spare
     tl.pf = 0;
-    for (int pf : {sb::C2PF, 6, 4, 3, 2})
-      if ((size_t)(pf + tl.ds) * band + obuf <= kSmemBudget) {
+    for (int pf : {sb::C2PF, 6, 4, 3, 2})  // slots of two bands each
+      if ((size_t)(2 * pf + tl.ds) * band + obuf <= kSmemBudget) {
         tl.pf = pf;
         break;
       }
     if (!tl.pf) continue;
-    tl.obuf_off = (int)((size_t)(tl.pf + tl.ds) * band);
+    tl.obuf_off = (int)((size_t)(2 * tl.pf + tl.ds) * band);
     *out = tl;
     return true;
   }
@@ -378,8 +378,8 @@ void make_output_map(float* dst, sb::Geometry& g, CUtensorMap* map) {
     g.out_bulk = 0;
 }
 
-// Tensor map of the int32 R plane [channel*batch][H][W] with a 16 x 128 box (the
-// prefix-form column kernel loads one band per TMA).  False when the plane rows
+// Tensor map of the int32 R plane [channel*batch][H][W] with a 32 x 128 box (the
+// prefix-form column kernel loads a pair of bands per TMA).  False when the plane rows
 // are not 16-byte multiples or no map can be made.
 bool make_plane_map(const int* mid, const sb::Geometry& g, int channels, CUtensorMap* map) {
   std::memset(map, 0, sizeof(*map));
@@ -387,7 +387,7 @@ bool make_plane_map(const int* mid, const sb::Geometry& g, int channels, CUtenso
   if (!enc || (g.mid_row * 4) % 16 != 0 || (g.mid_img * 4) % 16 != 0 || (uintptr_t)mid % 16 != 0) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.nimg * (cuuint64_t)channels};
   const cuuint64_t strides[2] = {(cuuint64_t)g.mid_row * 4, (cuuint64_t)g.mid_img * 4};
-  const cuuint32_t box[3] = {(cuuint32_t)sb::WS, (cuuint32_t)sb::HB, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)sb::WS, (cuuint32_t)(2 * sb::HB), 1};  // a pair of bands
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, (void*)mid, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==

@@ -1197,8 +1197,8 @@ __global__ void __launch_bounds__(C2THREADS, 1)
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const int D = tl.D, NB = D / HB, PF = tl.pf, DS = tl.ds;
   unsigned char* abase = smem + (((smem_u32(smem) + 127u) & ~127u) - smem_u32(smem));  // TMA: 128-byte aligned
-  int* lring = (int*)abase;                   // [PF][HB][WS] plane bands (TMA tensor loads)
-  int* dring = lring + PF * HB * WS;          // [DS][HB][WS] copies of old ring bands
+  int* lring = (int*)abase;                   // [PF][2][HB][WS] plane band pairs (TMA tensor loads)
+  int* dring = lring + PF * 2 * HB * WS;      // [DS][HB][WS] copies of old ring bands
   float* obuf = (float*)(abase + tl.obuf_off);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NB; ++i) mbar_init(&full[i], 32 * 4);
@@ -1223,8 +1223,9 @@ __global__ void __launch_bounds__(C2THREADS, 1)
     uint32_t onum = 0;
     int oob = 0;     // next output band to observe: index onum, band oob of segment so
     int slot = 0;
-    // plane bands arrive by TMA (one 16 x 128 box per band, issued PF-1 bands ahead by
-    // thread 0) into PF slots with full (tx bytes) / empty (one arrive per warp) barriers
+    // plane bands arrive in pairs by TMA (one 32 x 128 box, issued PF-1 pairs ahead by
+    // thread 0) into PF slots with full (tx bytes) / empty (one arrive per warp) barriers;
+    // a pair shares one lfull wait, one tcgen05.wait::st and one batch of copies
     int lslot = 0, islot = 0;
     uint32_t lph = 0, iph = 0;
     int cslot = tl.copy_e % NB, dslot = 0;  // ring slot (v + copy_e) % NB and copy slot of the next band copy
@@ -1233,23 +1234,25 @@ __global__ void __launch_bounds__(C2THREADS, 1)
       const long long mrow = g.mid_row;
       const int vstart = sc.a - 1 - t.pmax;
       const int zc = ch * g.nimg + sc.img;
-      auto issue = [&](int pb) {
-        if (threadIdx.x == 0 && pb < sc.nbands) {
+      const int npairs = (sc.nbands + 1) / 2;
+      auto issue = [&](int pp) {
+        if (threadIdx.x == 0 && pp < npairs) {
           mbar_wait(&lempty[islot], iph ^ 1);
-          mbar_expect_tx(&lfull[islot], HB * WS * 4);
-          tma_load_3d(lring + islot * (HB * WS), &mmap, x0, vstart + pb * HB, zc, &lfull[islot]);
+          mbar_expect_tx(&lfull[islot], 2 * HB * WS * 4);
+          tma_load_3d(lring + islot * (2 * HB * WS), &mmap, x0, vstart + pp * 2 * HB, zc, &lfull[islot]);
         }
-        if (pb < sc.nbands && ++islot == PF) {
+        if (pp < npairs && ++islot == PF) {
           islot = 0;
           iph ^= 1;
         }
       };
-      for (int pb = 0; pb < PF - 1; ++pb) issue(pb);
+      for (int pp = 0; pp < PF - 1; ++pp) issue(pp);
       int cprefix = 0;
-      for (int pb = 0; pb < sc.nbands; ++pb, ++v) {
-        issue(pb + PF - 1);
-        // every output band reading ring band v - NB from TMEM is done
-        while (so.valid && (long long)(so.gb0 + (uint32_t)oob) + tl.lag <= (long long)v) {
+      for (int pp = 0; pp < npairs; ++pp) {
+        issue(pp + PF - 1);
+        const int nbp = min(2, sc.nbands - 2 * pp);  // bands in this pair
+        // every output band reading ring bands v+d - NB from TMEM is done
+        while (so.valid && (long long)(so.gb0 + (uint32_t)oob) + tl.lag <= (long long)v + nbp - 1) {
           mbar_wait(&done[onum % C2DONE], (onum / C2DONE) & 1);
           ++onum;
           if (++oob == (so.b - so.a + HB - 1) / HB) {
@@ -1257,30 +1260,34 @@ __global__ void __launch_bounds__(C2THREADS, 1)
             oob = 0;
           }
         }
-        uint32_t cv[HB];
-        const int v0 = vstart + pb * HB;
+        uint32_t cv[2][HB];
         mbar_wait(&lfull[lslot], lph);
-        if (v0 >= 0 && v0 + HB <= g.H) {
-          const int* lp = lring + lslot * (HB * WS) + c;
-          int e[HB];
 #pragma unroll
-          for (int r = 0; r < HB; ++r) e[r] = lp[r * WS];
-          // running prefix with a two-element stride: odd entries chain by 3-input adds,
-          // even entries hang off them (dependency depth 9 instead of 16)
-          int odd = cprefix;
+        for (int d = 0; d < 2; ++d) {
+          if (d >= nbp) break;
+          const int v0 = vstart + (2 * pp + d) * HB;
+          if (v0 >= 0 && v0 + HB <= g.H) {
+            const int* lp = lring + lslot * (2 * HB * WS) + d * (HB * WS) + c;
+            int e[HB];
 #pragma unroll
-          for (int r = 0; r < HB; r += 2) {
-            cv[r] = (uint32_t)(odd + e[r]);
-            odd = odd + e[r] + e[r + 1];
-            cv[r + 1] = (uint32_t)odd;
-          }
-          cprefix = odd;
-        } else {
-          // rows beyond the image edges replicate the border row (filtering.py:10-13)
+            for (int r = 0; r < HB; ++r) e[r] = lp[r * WS];
+            // running prefix with a two-element stride: odd entries chain by 3-input adds,
+            // even entries hang off them (dependency depth 9 instead of 16)
+            int odd = cprefix;
 #pragma unroll
-          for (int r = 0; r < HB; ++r) {
-            cprefix += __ldg(mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
-            cv[r] = (uint32_t)cprefix;
+            for (int r = 0; r < HB; r += 2) {
+              cv[d][r] = (uint32_t)(odd + e[r]);
+              odd = odd + e[r] + e[r + 1];
+              cv[d][r + 1] = (uint32_t)odd;
+            }
+            cprefix = odd;
+          } else {
+            // rows beyond the image edges replicate the border row (filtering.py:10-13)
+#pragma unroll
+            for (int r = 0; r < HB; ++r) {
+              cprefix += __ldg(mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
+              cv[d][r] = (uint32_t)cprefix;
+            }
           }
         }
         __syncwarp();
@@ -1289,26 +1296,45 @@ __global__ void __launch_bounds__(C2THREADS, 1)
           lslot = 0;
           lph ^= 1;
         }
-        tmem_st16(tlane + (uint32_t)(slot * HB), cv);
-        if (slot == 0) tmem_st16(tlane + (uint32_t)D, cv);  // mirror: lag windows never wrap
+        const int slot0 = slot;
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          if (d >= nbp) break;
+          tmem_st16(tlane + (uint32_t)(slot * HB), cv[d]);
+          if (slot == 0) tmem_st16(tlane + (uint32_t)D, cv[d]);  // mirror: lag windows never wrap
+          if (++slot == NB) slot = 0;
+        }
         tmem_wait_st();
         tmem_fence_before();
-        mbar_arrive(&full[slot]);
-        if (++slot == NB) slot = 0;
+        mbar_arrive(&full[slot0]);
+        if (nbp == 2) mbar_arrive(&full[slot0 + 1 == NB ? 0 : slot0 + 1]);
         if (DS > 0) {
           // after releasing band v: copy band u = v - NB + copy_e out of the ring (its
           // readers wait for band v + 1 or later; see cols_prefix_tiling)
-          if ((long long)v >= (long long)NB - tl.copy_e) {
-            uint32_t old[HB];
-            tmem_ld16(tlane + (uint32_t)(cslot * HB), old);
-            tmem_wait_ld();
-            int* dp = dring + dslot * (HB * WS) + c;
+          uint32_t old[2][HB];
+          bool cp[2] = {false, false};
+          int cs = cslot;
 #pragma unroll
-            for (int r = 0; r < HB; ++r) dp[r * WS] = (int)old[r];
-            if (++dslot == DS) dslot = 0;
+          for (int d = 0; d < 2; ++d) {
+            if (d >= nbp) break;
+            cp[d] = (long long)v + d >= (long long)NB - tl.copy_e;
+            if (cp[d]) tmem_ld16(tlane + (uint32_t)(cs * HB), old[d]);
+            if (++cs == NB) cs = 0;
           }
-          if (++cslot == NB) cslot = 0;
+          tmem_wait_ld();
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            if (d >= nbp) break;
+            if (cp[d]) {
+              int* dp = dring + dslot * (HB * WS) + c;
+#pragma unroll
+              for (int r = 0; r < HB; ++r) dp[r * WS] = (int)old[d][r];
+              if (++dslot == DS) dslot = 0;
+            }
+            if (++cslot == NB) cslot = 0;
+          }
         }
+        v += (uint32_t)nbp;
       }
     }
   } else {
