@@ -96,6 +96,7 @@ struct Tiling {
   int deepmask;         // cols2: bit i = box i's trail window is read from the copies
   int lag;              // cols2: ring band v is written once output band v - lag is done
   int copy_e;           // cols2: band v - D/HB + copy_e is copied out of the ring while band v is written
+  int split;            // fused: 3 = three-CTA-per-SM variant (fused_kernel<uint8_t, K, 3>)
 };
 
 enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3, ColsPrefix = 4 };
@@ -913,8 +914,18 @@ constexpr int FPROD = 4;
 constexpr int FTHREADS = 32 * (FCONS + FPROD);
 constexpr int FPBUF = 2 * FPROD;
 
-template <typename Tin, int K>
-__global__ void __launch_bounds__(FTHREADS, 2)
+// MINB = 3 (uint8 one-channel float2 path): three CTAs per SM.  The kernel is compiled
+// for 80 registers per thread; the producer warpgroup gives registers back
+// (setmaxnreg.dec) so the consumer warpgroup can grow (setmaxnreg.inc), and the staged
+// band and the output staging box are single-buffered to fit three CTAs' shared memory.
+#ifndef SB_F3PREG
+#define SB_F3PREG 72
+#define SB_F3CREG 88
+#endif
+constexpr int F3PREG = SB_F3PREG, F3CREG = SB_F3CREG;
+
+template <typename Tin, int K, int MINB = 2>
+__global__ void __launch_bounds__(FTHREADS, MINB)
     fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status,
                  const __grid_constant__ CUtensorMap omap) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -932,9 +943,10 @@ __global__ void __launch_bounds__(FTHREADS, 2)
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const bool packed = (sizeof(Tin) == 1) && tl.packed;
+  constexpr int NSB = MINB == 3 ? 1 : 2;  // staged bands per producer warp
   const int pbuf_words = packed ? HB * LSP2 : HB * LS;  // packed: HB/2 float2 rows
-  unsigned char* stage = smem;                                        // FPROD producers x 2 staged bands
-  int* Pbase = (int*)(smem + 2 * FPROD * HB * tl.stage_row_bytes);    // FPROD x npb prefix buffers
+  unsigned char* stage = smem;                                          // FPROD producers x NSB staged bands
+  int* Pbase = (int*)(smem + NSB * FPROD * HB * tl.stage_row_bytes);    // FPROD x npb prefix buffers
   // FCONS x 2 output bands of HB x 32 floats (TMA stores; 128-byte aligned shared addresses)
   float* obuf = (float*)(smem + (((smem_u32(smem) + tl.obuf_off + 127u) & ~127u) - smem_u32(smem)));
   const int D = tl.D;
@@ -949,6 +961,12 @@ __global__ void __launch_bounds__(FTHREADS, 2)
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
+  if constexpr (MINB == 3) {
+    if (producer)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(F3PREG));
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(F3CREG));
+  }
 
   if (producer) {
     // ------------------------------------------------ producer warps
@@ -962,7 +980,7 @@ __global__ void __launch_bounds__(FTHREADS, 2)
     const int st_hi16 = g.aligned16 ? (st_hi & ~15) : st_hi;
     const int st_nchunk = max(0, (st_hi16 - st_lo) >> 4);
     const uint32_t st_magic = 0xFFFFFFFFu / (uint32_t)max(1, st_nchunk) + 1u;
-    unsigned char* mystage = stage + pw * 2 * HB * tl.stage_row_bytes;
+    unsigned char* mystage = stage + pw * NSB * HB * tl.stage_row_bytes;
     uint32_t gb0 = 0;  // global index of the segment's first band
     for (long long T = T0; T < T1;) {
       const int img = (int)(T / wh);
@@ -974,6 +992,7 @@ __global__ void __launch_bounds__(FTHREADS, 2)
       const int count = (b - a) + 2 * t.pmax + 1;
       const int nbands = (count + HB - 1) / HB;
       const int first = (int)(((uint32_t)pw + FPROD * 64u - gb0 % FPROD) % FPROD);  // first owned band
+      __syncwarp();  // every lane is done with the staged band (single-buffer case)
       if (first < nbands)
         issue_stage<Tin>(mystage, src_img, g, tl, xb, vstart + first * HB, min(HB, count - first * HB), st_lo,
                          st_nchunk, st_magic, st_hi16, st_hi, lane, 32);
@@ -981,10 +1000,10 @@ __global__ void __launch_bounds__(FTHREADS, 2)
       for (int pb = first; pb < nbands; pb += FPROD, sb ^= 1) {
         const uint32_t gb = gb0 + pb;
         const int n = min(HB, count - pb * HB);
-        unsigned char* cur = mystage + sb * HB * tl.stage_row_bytes;
+        unsigned char* cur = mystage + (NSB == 2 ? sb : 0) * HB * tl.stage_row_bytes;
         cp_async_wait_all();  // this band landed (the next one is issued below)
         __syncwarp();
-        if (pb + FPROD < nbands)
+        if (NSB == 2 && pb + FPROD < nbands)
           issue_stage<Tin>(mystage + (sb ^ 1) * HB * tl.stage_row_bytes, src_img, g, tl, xb,
                            vstart + (pb + FPROD) * HB, min(HB, count - (pb + FPROD) * HB), st_lo, st_nchunk, st_magic,
                            st_hi16, st_hi, lane, 32);
@@ -1008,6 +1027,12 @@ __global__ void __launch_bounds__(FTHREADS, 2)
             scan_rows<Tin>(cur, P, g, t, tl, ch, n, status, 0, 1);
           else
             scan_band8<Tin>(cur, P, g, t, tl, ch, n, status);
+        }
+        if (NSB == 1) {  // single staged band: the next one lands while the other producers' bands are used
+          __syncwarp();
+          if (pb + FPROD < nbands)
+            issue_stage<Tin>(mystage, src_img, g, tl, xb, vstart + (pb + FPROD) * HB, min(HB, count - (pb + FPROD) * HB),
+                             st_lo, st_nchunk, st_magic, st_hi16, st_hi, lane, 32);
         }
         mbar_arrive(&bar_full[pbi]);
       }
@@ -1082,8 +1107,13 @@ __global__ void __launch_bounds__(FTHREADS, 2)
             // stage the band (row r of this warp's 32 columns at ob[r][lane]) and let one
             // TMA tensor store write the 16 x 32 box: no per-row address arithmetic
             const int lane = threadIdx.x & 31;
-            float* ob = obuf + (warp * 2 + obsel) * (HB * 32);
-            if (lane == 0) bulk_wait_read<1>();  // the store out of this buffer (two bands ago) has read it
+            float* ob = obuf + (warp * NSB + (NSB == 2 ? obsel : 0)) * (HB * 32);
+            if (lane == 0) {  // the store out of this buffer (NSB bands ago) has read it
+              if (NSB == 2)
+                bulk_wait_read<1>();
+              else
+                bulk_wait_read<0>();
+            }
             __syncwarp();
 #pragma unroll
             for (int r = 0; r < HB; ++r) ob[r * 32 + lane] = ov[r];
@@ -1153,6 +1183,19 @@ struct SegIter {
     load();
   }
 };
+inline const void* fused3_ptr_for(int k) {
+  switch (k) {
+    case 1: return (const void*)fused_kernel<uint8_t, 1, 3>;
+    case 2: return (const void*)fused_kernel<uint8_t, 2, 3>;
+    case 3: return (const void*)fused_kernel<uint8_t, 3, 3>;
+    case 4: return (const void*)fused_kernel<uint8_t, 4, 3>;
+    case 5: return (const void*)fused_kernel<uint8_t, 5, 3>;
+    case 6: return (const void*)fused_kernel<uint8_t, 6, 3>;
+    case 7: return (const void*)fused_kernel<uint8_t, 7, 3>;
+    default: return (const void*)fused_kernel<uint8_t, 8, 3>;
+  }
+}
+
 constexpr int FRING = 32;  // max ring slots (512 TMEM columns / HB)
 
 // ---------------------------------------------------------------- column pass, prefix form (large radii)
@@ -1650,6 +1693,7 @@ int launch_filter_at(const void* src, int src_dtype, long long row_stride, int H
 const void* sweep_ptr_cols(int k);   // ColsFromMid (source type unused)
 const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)
+const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
 
 template <typename Tin>
 const void* sweep_ptr_for(Mode m, int k) {
