@@ -32,8 +32,10 @@
  *     uint8/uint16 input the first pass is exact; float input is quantised
  *     with a quantum derived from `value_bound` (an upper bound on |pixel|;
  *     pass <= 0 to declare "unknown", which the host wrapper resolves with a
- *     device max before calling).  Pixels violating the bound are reported
- *     through `status_dev` (bit SB_STATUS_RANGE) - never silently.
+ *     device max before calling).  For uint16 input a value_bound in
+ *     (0, 65535) only refines the row-value quantum (the samples stay exact).
+ *     Pixels violating the bound are reported through `status_dev` (bit
+ *     SB_STATUS_RANGE) - never silently.
  *   - Return value: SB_OK or an error code; the message is in sb_last_error().
  */
 #ifndef SLICEBLUR_B200_H

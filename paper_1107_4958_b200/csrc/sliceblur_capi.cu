@@ -68,7 +68,11 @@ int make_taps(const int64_t* radii, const double* weights, int k, int src_dtype,
   double bound;
   switch (src_dtype) {
     case SB_DTYPE_U8: bound = 255.0; break;
-    case SB_DTYPE_U16: bound = 65535.0; break;
+    case SB_DTYPE_U16:
+      // uint16 samples enter exactly; a caller bound below 65535 (e.g. a 12-bit PGM's maxval)
+      // only refines the row-value quantum, and samples above it are reported, never used
+      bound = (value_bound > 0.0 && value_bound < 65535.0) ? std::ceil(value_bound) : 65535.0;
+      break;
     case SB_DTYPE_F32:
     case SB_DTYPE_F64:
       if (!(value_bound >= 0.0) || !std::isfinite(value_bound))
@@ -103,7 +107,7 @@ int make_taps(const int64_t* radii, const double* weights, int k, int src_dtype,
     t.w_out1[i] = (float)std::ldexp(weights[i], -s_in);
   }
   t.in_scale = (float)std::ldexp(1.0, s_in);
-  t.in_limit = 4194304.0f;
+  t.in_limit = src_dtype == SB_DTYPE_U16 ? (float)bound : 4194304.0f;  // uint16: largest admissible sample
   plan->pmax = pmax;
   return SB_OK;
 }

@@ -254,6 +254,7 @@ __device__ __forceinline__ int to_fixed(T v, const Taps& t, bool& bad) {
     s = ok ? s : 0.0f;
     return __float_as_int(s + kMagic) - kMagicBits;  // round-to-nearest-even of v * 2^s_in
   } else {
+    if constexpr (sizeof(T) == 2) bad |= (float)v > t.in_limit;  // uint16 above the caller's bound
     return (int)v;
   }
 }

@@ -126,8 +126,14 @@ class _Device:
         self.stream = torch.cuda.current_stream().cuda_stream
 
     def value_bound(self, given):
-        if self.code in (nat.SB_DTYPE_U8, nat.SB_DTYPE_U16):
+        if self.code == nat.SB_DTYPE_U8:
             return 0.0  # exact integer path; bound implied by the dtype
+        if self.code == nat.SB_DTYPE_U16 and given is None:
+            # exact samples either way; the measured maximum only refines the row-value quantum
+            out = self.torch.zeros(1, dtype=self.torch.float64, device=self.tensor.device)
+            _raise_for(nat.load().sb_max_abs(self.tensor.data_ptr(), self.code, self.tensor.numel(), out.data_ptr(),
+                                              self.stream))
+            return max(1.0, float(out.item()))
         if given is not None:
             return float(given)
         out = self.torch.zeros(1, dtype=self.torch.float64, device=self.tensor.device)
