@@ -13,7 +13,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "sliceblur_b200.h"
 #include "sweep_kernels.cuh"
@@ -277,6 +279,59 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
   return false;
 }
 
+// Immutable launch facts, looked up once per (kernel, device) instead of on every call
+// (small images are host-bound otherwise): register count, static shared memory, the
+// dynamic shared memory already granted with cudaFuncSetAttribute, and the device's SM
+// count / shared memory / register file.  Guarded by a mutex; entries are never removed.
+struct FnFacts {
+  const void* fn;
+  int dev;
+  int num_regs;
+  size_t static_smem;
+  size_t granted;
+};
+struct DevFacts {
+  int sms, smem_per_sm, regs_per_sm;
+};
+std::mutex g_facts_mu;
+std::vector<FnFacts> g_fn_facts;
+DevFacts g_dev_facts[64];
+bool g_dev_known[64];
+
+int launch_facts(const void* fn, size_t smem, FnFacts* ff, DevFacts* df) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(g_facts_mu);
+  FnFacts* f = nullptr;
+  for (auto& x : g_fn_facts)
+    if (x.fn == fn && x.dev == dev) f = &x;
+  if (!f) {
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+    g_fn_facts.push_back({fn, dev, fa.numRegs, fa.sharedSizeBytes, 0});
+    f = &g_fn_facts.back();
+  }
+  if (smem > f->granted) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    f->granted = smem;
+  }
+  *ff = *f;
+  if (dev < 0 || dev >= 64) return fail(SB_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+  if (!g_dev_known[dev]) {
+    DevFacts d{148, 233472, 65536};
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&d.regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    g_dev_facts[dev] = d;
+    g_dev_known[dev] = true;
+  }
+  *df = g_dev_facts[dev];
+  return SB_OK;
+}
+
 int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, int W, long long total_rows,
                 int channels, Launch* out) {
   sb::Tiling& tl = out->tl;
@@ -286,23 +341,18 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, in
   if (smem > 227 * 1024)
     return fail(SB_ERR_INVALID_ARGUMENT, "slice radius " + std::to_string(pmax) + " too large for the GPU strip sweep");
   out->smem = smem;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-  int dev = 0, sms = 148, occ = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  FnFacts fa;
+  DevFacts df;
+  int rc = launch_facts(fn, smem, &fa, &df);
+  if (rc) return rc;
+  int occ = 1;
+  const int sms = df.sms, smem_per_sm = df.smem_per_sm, regs_per_sm = df.regs_per_sm;
   // Residency from the kernel's own resources.  (cudaOccupancyMaxActiveBlocksPerMultiprocessor
   // reports 1 for kernels that allocate tensor memory, which would idle 3/4 of each SM.)
-  cudaFuncAttributes fa;
-  e = cudaFuncGetAttributes(&fa, fn);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
-  int smem_per_sm = 233472, regs_per_sm = 65536;
-  cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  cudaDeviceGetAttribute(&regs_per_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
   const int threads = (m == sb::Mode::Fused) ? sb::FTHREADS : (m == sb::Mode::ColsPrefix ? sb::C2THREADS : sb::WS);
-  const int regs_per_cta = ((fa.numRegs * 32 + 255) / 256) * 256 * (threads / 32);
+  const int regs_per_cta = ((fa.num_regs * 32 + 255) / 256) * 256 * (threads / 32);
   occ = std::min(2048 / threads, regs_per_sm / std::max(1, regs_per_cta));
-  occ = std::min<long long>(occ, (long long)smem_per_sm / (long long)(smem + fa.sharedSizeBytes + 1024));
+  occ = std::min<long long>(occ, (long long)smem_per_sm / (long long)(smem + fa.static_smem + 1024));
   if (m == sb::Mode::Fused || m == sb::Mode::ColsFromMid || m == sb::Mode::ColsPrefix)
     occ = std::min(occ, 512 / tl.tmem_cols);
   occ = std::max(occ, 1);
@@ -360,18 +410,16 @@ int launch_cols(const void* fn, const Launch& L, const int* mid_in, float* dst, 
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda at link time)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // looked up once (thread-safe static initialisation)
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     cudaDriverEntryPointQueryResult q;
     void* p = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-    else
-      cudaGetLastError();
-  }
+      return (PFN_cuTensorMapEncodeTiled_v12000)p;
+    cudaGetLastError();
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 

@@ -59,15 +59,36 @@ _DTYPE_CODES = {
 }
 
 
-def _kernel_arrays(kernel: SliceKernel):
+# SliceKernel is immutable: its contiguous arrays, ctypes pointers and DC gain are
+# computed once per kernel object (small images are host-bound otherwise).  The cache
+# holds the kernel itself, so an id() is never reused while its entry exists.
+_KERNEL_CACHE: "dict[int, tuple]" = {}
+_KERNEL_CACHE_MAX = 64
+
+
+def _kernel_info(kernel: SliceKernel):
+    hit = _KERNEL_CACHE.get(id(kernel))
+    if hit is not None and hit[0] is kernel:
+        return hit
     radii = np.ascontiguousarray(kernel.radii, dtype=np.int64)
     weights = np.ascontiguousarray(kernel.weights, dtype=np.float64)
-    return (
+    info = (
+        kernel,
         radii,
         weights,
         radii.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
         weights.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+        int(kernel.max_radius),
+        float(kernel.dc_gain),
     )
+    if len(_KERNEL_CACHE) >= _KERNEL_CACHE_MAX:
+        _KERNEL_CACHE.clear()
+    _KERNEL_CACHE[id(kernel)] = info
+    return info
+
+
+def _kernel_arrays(kernel: SliceKernel):
+    return _kernel_info(kernel)[1:5]
 
 
 def _raise_for(code: int):
@@ -83,9 +104,10 @@ def _raise_for(code: int):
 
 def _check_kernel(kernel: SliceKernel, n: int):
     """Mirror of filtering.py:39-45 (also enforced again inside the C ABI)."""
-    if kernel.max_radius >= n:
-        raise KernelTooLargeError(f"slice radius {kernel.max_radius} does not fit extent {n}")
-    if abs(kernel.dc_gain - 1.0) > _DC_TOL:
+    info = _kernel_info(kernel)
+    if info[5] >= n:
+        raise KernelTooLargeError(f"slice radius {info[5]} does not fit extent {n}")
+    if abs(info[6] - 1.0) > _DC_TOL:
         raise ValueError("kernel must have unit DC gain; call normalized()")
     if kernel.k > nat.SB_MAX_K:
         raise ValueError(f"at most {nat.SB_MAX_K} slices are supported on the GPU path")
@@ -94,11 +116,15 @@ def _check_kernel(kernel: SliceKernel, n: int):
 class _Device:
     """Moves an input to the GPU (if needed) and remembers how to return the result."""
 
+    _ready = False
+
     def __init__(self, data):
         torch = _torch()
-        if not torch.cuda.is_available():
-            raise RuntimeError("sliceblur_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
-        nat.load()
+        if not _Device._ready:
+            if not torch.cuda.is_available():
+                raise RuntimeError("sliceblur_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+            nat.load()
+            _Device._ready = True
         self.torch = torch
         self.host_tensor = False
         if isinstance(data, torch.Tensor):
@@ -205,15 +231,17 @@ def separable_filter_batch(images, kernel: SliceKernel, *, channels_last: bool =
         result = torch.empty(tuple(dev.tensor.shape), dtype=torch.float32, device=x.device)
     radii, weights, rp, wp = _kernel_arrays(kernel)
     lib = nat.load()
-    ws_bytes = lib.sb_separable_filter_2d_workspace_bytes(dev.code, b, h, w, c, rp, kernel.k)
-    workspace = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=x.device)
-    status = torch.zeros(1, dtype=torch.int32, device=x.device)
+    ws_bytes = int(lib.sb_separable_filter_2d_workspace_bytes(dev.code, b, h, w, c, rp, kernel.k))
+    workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device) if ws_bytes else None
+    # the range status word is only read when checking (the kernels skip it when NULL)
+    status = torch.zeros(1, dtype=torch.int32, device=x.device) if check else None
     bound = dev.value_bound(value_bound)
     code = lib.sb_separable_filter_2d(
         x.data_ptr(), dev.code, b, h, w, c, h * w * c, w * c,
         result.data_ptr(), h * w * c, w * c,
         rp, wp, kernel.k, bound,
-        workspace.data_ptr(), int(ws_bytes), status.data_ptr(), dev.stream,
+        workspace.data_ptr() if workspace is not None else None, ws_bytes,
+        status.data_ptr() if status is not None else None, dev.stream,
     )
     _raise_for(code)
     return dev.finish(result, status, check, host_out)
