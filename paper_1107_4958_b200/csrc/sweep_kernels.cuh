@@ -1411,20 +1411,32 @@ __global__ void __launch_bounds__(C2THREADS, 1)
         tmem_fence_after();
         const int base = (int)(j % (uint32_t)NB) * HB;  // ring position of virtual row 16*ob
         float2 o2[HB / 2];
+        // boxes in pairs: both boxes' TMEM windows are in flight under one tcgen05.wait
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          uint32_t lv[HB], tv[HB];
+        for (int i0 = 0; i0 < K; i0 += 2) {
+        uint32_t lvp[2][HB], tvp[2][HB];
+#pragma unroll
+        for (int d2 = 0; d2 < 2; ++d2) {
+          const int i = i0 + d2;
+          if (i >= K) break;
           int l = base + t.pmax + 1 + t.p[i];
           l = l >= D ? l - D : l;
           l = l >= D ? l - D : l;
-          tmem_ld16(tlane + (uint32_t)l, lv);
-          const bool deep = (tl.deepmask >> i) & 1;
-          if (!deep) {
+          tmem_ld16(tlane + (uint32_t)l, lvp[d2]);
+          if (!((tl.deepmask >> i) & 1)) {
             int tr = base + t.pmax - t.p[i];
             tr = tr >= D ? tr - D : tr;
-            tmem_ld16(tlane + (uint32_t)tr, tv);
+            tmem_ld16(tlane + (uint32_t)tr, tvp[d2]);
           }
-          tmem_wait_ld();
+        }
+        tmem_wait_ld();
+#pragma unroll
+        for (int d2 = 0; d2 < 2; ++d2) {
+          const int i = i0 + d2;
+          if (i >= K) break;
+          uint32_t (&lv)[HB] = lvp[d2];
+          uint32_t (&tv)[HB] = tvp[d2];
+          const bool deep = (tl.deepmask >> i) & 1;
           if (deep) {
             // virtual rows 16*ob + pmax - p_i .. +15 from the band copies (band j + off/16 on)
             const int off = t.pmax - t.p[i];
@@ -1450,6 +1462,7 @@ __global__ void __launch_bounds__(C2THREADS, 1)
             const float2 d = make_float2(i2f_fast(lv[2 * r] - tv[2 * r]), i2f_fast(lv[2 * r + 1] - tv[2 * r + 1]));
             o2[r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, o2[r]);
           }
+        }
         }
         tmem_fence_before();
         mbar_arrive(&done[onum % C2DONE]);
