@@ -179,11 +179,20 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
   while (cols < tl.D + sb::HB) cols <<= 1;
   tl.tmem_cols = cols;
   if (m == sb::Mode::Fused && tl.packed == 1) {
-    // fused_kernel<uint8_t, K, 3>: three CTAs per SM (registers rebalanced between the
-    // producer and consumer warpgroups with setmaxnreg), single-buffered staging and output
-    // box.  SB_FUSED=1 keeps the two-CTA kernel (A/B).
+    // Default (SB_FUSED=5): fused_kernel<uint8_t, K, 2, true>, consumers take two bands per
+    // iteration (one prefix carry, one 32-column TMEM store, 32-row output bands).
+    // SB_FUSED=3: fused_kernel<uint8_t, K, 3>, three CTAs per SM (registers rebalanced between
+    // the producer and consumer warpgroups with setmaxnreg, single-buffered staging and output
+    // box).  SB_FUSED=1: the two-CTA one-band kernel.  (A/B switches.)
     const char* fe = std::getenv("SB_FUSED");
-    if (!fe || std::atoi(fe) == 3) {
+    if (!fe || std::atoi(fe) == 5) {
+      // two bands per consumer iteration: 32-row ring slots, 32-row mirror
+      tl.split = 5;
+      tl.D = ((2 * pmax + 65 + 31) / 32) * 32;
+      int cols5 = 32;
+      while (cols5 < tl.D + 32) cols5 <<= 1;
+      tl.tmem_cols = cols5;
+    } else if (std::atoi(fe) == 3) {
       tl.split = 3;
       const size_t end = (size_t)sb::FPROD * sb::HB * tl.stage_row_bytes +
                          (size_t)sb::FPROD * (sb::HB / 2) * sb::LSP2 * sizeof(float2);
@@ -205,7 +214,9 @@ size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
   if (m == sb::Mode::Fused) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
     // + FCONS x 2 output bands of HB x 32 floats staged for TMA tensor stores
-    size_t s = (size_t)tl.obuf_off + 128 + (size_t)sb::FCONS * (tl.split == 3 ? 1 : 2) * sb::HB * 32 * sizeof(float);
+    // output staging per consumer warp: 1 (three-CTA), 2 (two-CTA) 16-row boxes, or two 32-row boxes (split 5)
+    const int boxes = tl.split == 3 ? 1 : (tl.split == 5 ? 4 : 2);
+    size_t s = (size_t)tl.obuf_off + 128 + (size_t)sb::FCONS * boxes * sb::HB * 32 * sizeof(float);
     // cap residency at 512 / tmem_cols CTAs per SM by asking for enough shared
     // memory, so no CTA ever waits inside tcgen05.alloc
     return std::max(s, residency_floor(512 / tl.tmem_cols));
@@ -580,7 +591,9 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
 
   const size_t need = sb_separable_filter_2d_workspace_bytes(src_dtype, batch, height, width, channels, radii, k);
   if (need == 0) {
-    const void* fn = base.split == 3 ? sb::sweep_ptr_fused3(k) : pick_kernel(sb::Mode::Fused, src_dtype, k);
+    const void* fn = base.split == 3   ? sb::sweep_ptr_fused3(k)
+                     : base.split == 5 ? sb::sweep_ptr_fused5(k)
+                                       : pick_kernel(sb::Mode::Fused, src_dtype, k);
     Launch L;
     rc = plan_launch(fn, sb::Mode::Fused, base, plan.pmax, g.W, total_rows, channels, &L);
     if (rc) return rc;

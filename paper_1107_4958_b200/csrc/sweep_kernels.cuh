@@ -181,6 +181,27 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 
 // ---- mbarriers (producer/consumer hand-off inside a CTA)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -925,7 +946,7 @@ constexpr int FPBUF = 2 * FPROD;
 #endif
 constexpr int F3PREG = SB_F3PREG, F3CREG = SB_F3CREG;
 
-template <typename Tin, int K, int MINB = 2>
+template <typename Tin, int K, int MINB = 2, bool B2 = false>
 __global__ void __launch_bounds__(FTHREADS, MINB)
     fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status,
                  const __grid_constant__ CUtensorMap omap) {
@@ -1039,6 +1060,115 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
       }
       gb0 += (uint32_t)nbands;
     }
+  } else if constexpr (B2) {
+    // ------------------------------------------------ consumer warps, two bands per iteration
+    // (uint8 packed path): one prefix carry, one 32-column TMEM store, one 32-row output band
+    // with 32-row TMEM windows and one staged 32 x 32 box per iteration
+    const int c = threadIdx.x, lane = threadIdx.x & 31;
+    const bool active = (x0 + c) < g.W;
+    const uint32_t tlane = tmem_base_s + ((uint32_t)(threadIdx.x & ~31) << 16);
+    uint32_t gb = 0;
+    int obsel = 0;
+    for (long long T = T0; T < T1;) {
+      const int img = (int)(T / wh);
+      const int a = g.oy0 + (int)(T - (long long)img * wh);
+      const int b = g.oy0 + (int)min((long long)wh, T1 - (long long)img * wh);
+      T = (long long)img * wh + (b - g.oy0);
+      const int count = (b - a) + 2 * t.pmax + 1;
+      const int nbands = (count + HB - 1) / HB;
+      int out_next = a, out_mod = 0, prod_slot = 0;
+      int cprefix = 0;
+      for (int pb = 0; pb < nbands; pb += 2) {
+        uint32_t cv[2 * HB];
+        int produced = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (pb + h < nbands) {
+            const uint32_t kb = gb / FPROD;
+            const int pbi = (int)(gb % FPROD) * tl.npb + (int)(kb & (uint32_t)(tl.npb - 1));
+            const float2* P = (const float2*)(Pbase + pbi * pbuf_words);
+            mbar_wait(&bar_full[pbi], (kb >> (tl.npb - 1)) & 1);
+            float2 r2[HB / 2];
+            band_rows_f2<K>(P, c, t, tl, r2);
+            mbar_arrive(&bar_empty[pbi]);
+#pragma unroll
+            for (int q = 0; q < HB / 2; ++q) {
+              r2[q] = __fadd2_rn(r2[q], make_float2(kMagic, kMagic));  // round to the mid quantum
+              cv[h * HB + q] = __float_as_uint(r2[q].x);
+              cv[h * HB + q + HB / 2] = __float_as_uint(r2[q].y);
+            }
+            produced = (pb + h) * HB + min(HB, count - (pb + h) * HB);
+            ++gb;
+          } else {
+#pragma unroll
+            for (int q = 0; q < HB; ++q) cv[h * HB + q] = (uint32_t)kMagicBits;  // zero rows past the end
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 2 * HB; ++r) {
+          cprefix += (int)cv[r] - kMagicBits;
+          cv[r] = (uint32_t)cprefix;
+        }
+        tmem_st32(tlane + (uint32_t)prod_slot, cv);
+        if (prod_slot == 0) tmem_st32(tlane + (uint32_t)D, cv);  // 32-row mirror
+        tmem_wait_st();
+        prod_slot += 2 * HB;
+        prod_slot = prod_slot >= D ? 0 : prod_slot;
+        while (out_next < b) {
+          const int nb = min(2 * HB, b - out_next);
+          if (produced < (out_next - a) + nb + 2 * t.pmax + 1) break;
+          float2 o2[HB];
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            int l = out_mod + t.pmax + 1 + t.p[i];
+            int tr = out_mod + t.pmax - t.p[i];
+            l = l >= D ? l - D : l;
+            tr = tr >= D ? tr - D : tr;
+            uint32_t lv[2 * HB], tv[2 * HB];
+            tmem_ld32(tlane + (uint32_t)l, lv);
+            tmem_ld32(tlane + (uint32_t)tr, tv);
+            tmem_wait_ld();
+            const float2 w2 = make_float2(t.w_col[i], t.w_col[i]);
+#pragma unroll
+            for (int r = 0; r < HB; ++r) {
+              const float2 d = make_float2(i2f_fast(lv[2 * r] - tv[2 * r]), i2f_fast(lv[2 * r + 1] - tv[2 * r + 1]));
+              o2[r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, o2[r]);
+            }
+          }
+          if (g.out_bulk && nb == 2 * HB) {
+            float* ob = obuf + (warp * 2 + obsel) * (2 * HB * 32);
+            if (lane == 0) bulk_wait_read<1>();  // the stores out of this box (two bands ago) have read it
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < HB; ++r) {
+              ob[(2 * r) * 32 + lane] = o2[r].x;
+              ob[(2 * r + 1) * 32 + lane] = o2[r].y;
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&omap, ob, x0 + (warp << 5), out_next - g.oy0, img);
+              tma_store_3d(&omap, ob + HB * 32, x0 + (warp << 5), out_next + HB - g.oy0, img);
+              bulk_commit();
+            }
+            obsel ^= 1;
+          } else if (active) {
+            float* dptr = dst + (long long)img * g.out_img + (long long)(out_next - g.oy0) * g.out_row + (x0 + c);
+#pragma unroll
+            for (int r = 0; r < HB; ++r) {
+              if (2 * r < nb) st_stream(dptr, o2[r].x);
+              dptr += g.out_row;
+              if (2 * r + 1 < nb) st_stream(dptr, o2[r].y);
+              dptr += g.out_row;
+            }
+          }
+          out_next += nb;
+          out_mod += nb;
+          out_mod = out_mod >= D ? out_mod - D : out_mod;
+        }
+      }
+    }
+    if ((threadIdx.x & 31) == 0) bulk_wait_read<0>();
   } else {
     // ------------------------------------------------ consumer warps
     const int c = threadIdx.x;
@@ -1184,6 +1314,19 @@ struct SegIter {
     load();
   }
 };
+inline const void* fused5_ptr_for(int k) {
+  switch (k) {
+    case 1: return (const void*)fused_kernel<uint8_t, 1, 2, true>;
+    case 2: return (const void*)fused_kernel<uint8_t, 2, 2, true>;
+    case 3: return (const void*)fused_kernel<uint8_t, 3, 2, true>;
+    case 4: return (const void*)fused_kernel<uint8_t, 4, 2, true>;
+    case 5: return (const void*)fused_kernel<uint8_t, 5, 2, true>;
+    case 6: return (const void*)fused_kernel<uint8_t, 6, 2, true>;
+    case 7: return (const void*)fused_kernel<uint8_t, 7, 2, true>;
+    default: return (const void*)fused_kernel<uint8_t, 8, 2, true>;
+  }
+}
+
 inline const void* fused3_ptr_for(int k) {
   switch (k) {
     case 1: return (const void*)fused_kernel<uint8_t, 1, 3>;
@@ -1708,6 +1851,7 @@ const void* sweep_ptr_cols(int k);   // ColsFromMid (source type unused)
 const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)
 const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
+const void* sweep_ptr_fused5(int k);      // fused sweep, two bands per consumer iteration (uint8, one channel)
 
 template <typename Tin>
 const void* sweep_ptr_for(Mode m, int k) {
