@@ -1788,31 +1788,47 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
         const int img = (int)(trow / g.H), v = (int)(trow - (long long)img * g.H);
         midrow[r] = mid_out + ch * g.mid_ch + (long long)img * g.mid_img + (long long)v * g.mid_row;
       }
-      for (int o = 0; o < nout; ++o) {
-        const uint32_t gj = cin_ctr + min(o + lagc, nin - 1);  // chunks complete in order
+      // two output chunks per iteration: one wait (chunks complete in order), both chunks'
+      // row values in flight together, then both done-arrivals and stores
+      for (int o = 0; o < nout; o += 2) {
+        const int no = min(2, nout - o);
+        const uint32_t gj = cin_ctr + min(o + no - 1 + lagc, nin - 1);
         mbar_wait(&bar_full[gj % NSLOT], (gj / NSLOT) & 1);
-        const int x = o * CW + c;
-        float2 rv[HB / 2];  // rows (2r, 2r+1): packed FMUL2 / FFMA2 / FADD2
+        float2 rv[2][HB / 2];  // rows (2r, 2r+1) of chunks o, o+1: packed FMUL2 / FFMA2 / FADD2
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          const int* pl = P + ((x - xs + t.p[i]) & (RL - 1));
-          const int* pt = P + ((x - xs - t.p[i] - 1) & (RL - 1));
-          const float2 w2 = make_float2(t.w_row[i], t.w_row[i]);
+        for (int h = 0; h < 2; ++h) {
+          if (h >= no) break;
+          const int x = (o + h) * CW + c;
 #pragma unroll
-          for (int r = 0; r < HB / 2; ++r) {
-            const float2 d = make_float2(i2f_fast((uint32_t)(pl[2 * r * RLS] - pt[2 * r * RLS])),
-                                         i2f_fast((uint32_t)(pl[(2 * r + 1) * RLS] - pt[(2 * r + 1) * RLS])));
-            rv[r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, rv[r]);
+          for (int i = 0; i < K; ++i) {
+            const int* pl = P + ((x - xs + t.p[i]) & (RL - 1));
+            const int* pt = P + ((x - xs - t.p[i] - 1) & (RL - 1));
+            const float2 w2 = make_float2(t.w_row[i], t.w_row[i]);
+#pragma unroll
+            for (int r = 0; r < HB / 2; ++r) {
+              const float2 d = make_float2(i2f_fast((uint32_t)(pl[2 * r * RLS] - pt[2 * r * RLS])),
+                                           i2f_fast((uint32_t)(pl[(2 * r + 1) * RLS] - pt[(2 * r + 1) * RLS])));
+              rv[h][r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, rv[h][r]);
+            }
           }
         }
-        const uint32_t go = out_ctr + o;
-        mbar_arrive(&bar_done[go % NSLOT]);
-        if (x < g.W) {
 #pragma unroll
-          for (int r = 0; r < HB / 2; ++r) {
-            const float2 q = __fadd2_rn(rv[r], make_float2(kMagic, kMagic));  // round to the mid quantum
-            if (2 * r < nrows) midrow[2 * r][x] = __float_as_int(q.x) - kMagicBits;
-            if (2 * r + 1 < nrows) midrow[2 * r + 1][x] = __float_as_int(q.y) - kMagicBits;
+        for (int h = 0; h < 2; ++h) {
+          if (h >= no) break;
+          const uint32_t go = out_ctr + o + h;
+          mbar_arrive(&bar_done[go % NSLOT]);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h >= no) break;
+          const int x = (o + h) * CW + c;
+          if (x < g.W) {
+#pragma unroll
+            for (int r = 0; r < HB / 2; ++r) {
+              const float2 q = __fadd2_rn(rv[h][r], make_float2(kMagic, kMagic));  // round to the mid quantum
+              if (2 * r < nrows) midrow[2 * r][x] = __float_as_int(q.x) - kMagicBits;
+              if (2 * r + 1 < nrows) midrow[2 * r + 1][x] = __float_as_int(q.y) - kMagicBits;
+            }
           }
         }
       }
