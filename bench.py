@@ -5,21 +5,29 @@
 Workload (default c3 = BASELINE.json configs[2]): a batch of 256 uint8
 1024x1024 one-over-f images filtered with sigma=10, K=3 table boxes
 (radii 7/14/23) into float32 - the config the metric's 1/2/4/8-GPU scaling is
-quoted on.  Multi-GPU: one process per GPU (torchrun), every rank filters its
-own 256-image batch (weak scaling, no data-path collective); timing is CUDA
-events on the launching stream, max over ranks.
+quoted on.  Multi-GPU: one process per GPU; ``--gpus N`` re-launches itself
+under torchrun when started as a single process.  C3 shards BASELINE's 256
+images over the ranks (256/N each, no data-path collective: strong scaling);
+C5 splits the 32768^2 image into row strips with NCCL halo exchange.  Timing is
+CUDA events on the launching stream, max over ranks.
 
-* ``value``    - Mpixels/s over all ranks with inputs resident in HBM
-                 (inputs 268 MB + outputs 1 GB per rank > 126 MB L2, so no flush
-                 is needed between steps);
-* ``e2e``      - the same metric through the public API
-                 (``separable_filter_batch``) from pinned host memory, H2D of
-                 the input and D2H of the filtered images inside the timed region;
+* ``value``    - Mpixels/s of the whole job with inputs resident in HBM (each
+                 step replays a CUDA graph of the public call, so launch overhead
+                 does not hide in small per-GPU shards; inputs + outputs exceed
+                 the 126 MB L2, so no flush is needed between steps);
+* ``e2e``      - the same metric through the public API from pinned host memory,
+                 H2D of the input and D2H of the filtered images inside the timed
+                 region (C3: ``separable_filter_batch``; float configs: the
+                 reference signature ``separable_filter_2d(img, kern)`` with no
+                 value_bound);
 * ``roofline`` - algorithmic bytes (1 read of the input + 1 write of the output
-                 per pixel) per launch / CUDA-event launch time vs the measured
-                 HBM copy peak (MEASURED_PEAKS.json);
-* ``cpu_baseline`` - the reference algorithm's numpy port (oracle/), all host
-                 cores, on a bounded sample, rank 0 at N=1.
+                 per pixel) per step / CUDA-event step time vs the measured HBM
+                 copy peak (MEASURED_PEAKS.json);
+* ``cpu_baseline`` - the shipped reference (``baseline/_ref``, installed from
+                 /root/reference; else the oracle's numpy port) on the box's host
+                 cores, rank 0 at N=1, on a bounded sample: serial, its own
+                 ``parallel=True`` (4 threads) and an all-core row-block pool over
+                 its ``_filter_rows`` (bit-identical), medians of 3.
 
 ``--impl reference`` times that CPU implementation alone (rank 0; other ranks
 exit 0) on the same metric/config.
@@ -141,15 +149,19 @@ def _dist():
     return world, rank, local
 
 
-def make_inputs(cfg, seed_base, device):
-    """Seeded synthetic inputs of the config, generated on the GPU (torch.fft)."""
+def make_inputs(cfg, seed_base, device, count=None):
+    """Seeded synthetic inputs of the config, generated on the GPU (torch.fft).
+
+    uint8 batches: image i (of ``count``, default the config's batch) uses seed
+    ``seed_base + i``; float configs: channel c uses ``seed_base + c``."""
     import torch
 
     from paper_1107_4958_b200 import synth
 
     if cfg["dtype"] == "u8":
-        out = torch.empty((cfg["batch"], cfg["h"], cfg["w"]), dtype=torch.uint8, device=device)
-        for i in range(cfg["batch"]):
+        n = cfg["batch"] if count is None else count
+        out = torch.empty((n, cfg["h"], cfg["w"]), dtype=torch.uint8, device=device)
+        for i in range(n):
             out[i] = synth.one_over_f_torch(cfg["h"], cfg["w"], seed_base + i, device=device).round_().to(torch.uint8)
         return out
     if cfg["channels"] == 1:
@@ -160,38 +172,123 @@ def make_inputs(cfg, seed_base, device):
     return out
 
 
-def cpu_reference_rate(cfg, sample_px_target: float, threads: int, reps: int = 1):
-    """Time the reference algorithm's numpy port (oracle/) on a bounded sample.
+def count_kernels(step):
+    """Names of the kernels one call of ``step`` launches (torch.profiler / CUPTI)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
 
-    Returns (Mpx/s, sample description).  Uses a thread pool over row blocks
-    like the reference's parallel=True (filtering.py:91-101), on ``threads`` cores.
-    """
-    from oracle import oracle
+    try:
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if str(e.device_type).endswith("CUDA")]
+    except Exception:  # pragma: no cover - CUPTI unavailable
+        return None
+    return [n for n in names if not n.lower().startswith(("memcpy", "memset"))]
+
+
+def _reference_module():
+    """The shipped reference (baseline/_ref/sliceblur), or None when it is not installed."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "sliceblur")):
+        return None
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    try:
+        import sliceblur.approx as ra
+        import sliceblur.filtering as rf
+    except Exception:  # pragma: no cover - depends on the install
+        return None
+    return ra, rf
+
+
+def _reference_arms(cfg):
+    """Callables (name, threads, fn(img)) of the three CPU arms, and the kind."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    threads = len(os.sched_getaffinity(0))
+    mods = _reference_module()
+    if mods is not None:
+        ra, rf = mods
+        kern = ra.scale_to_sigma(ra.to_slices(*ra.table_defaults(cfg["k"])), cfg["sigma"])
+
+        def rows(a):
+            return rf._filter_rows(a, kern)
+
+        def serial(img):
+            return rf.separable_filter_2d(img, kern)
+
+        def par4(img):
+            return rf.separable_filter_2d(img, kern, parallel=True)
+        kind = "reference"
+    else:
+        from oracle import oracle
+        from paper_1107_4958_b200 import table_kernel
+
+        k2 = table_kernel(cfg["k"], cfg["sigma"])
+
+        def rows(a):
+            return oracle.np_filter_rows(a, k2.radii, k2.weights)
+
+        def serial(img):
+            return oracle.np_separable_filter_2d(img, k2.radii, k2.weights, threads=1)
+
+        def par4(img):
+            return oracle.np_separable_filter_2d(img, k2.radii, k2.weights, threads=4)
+        kind = "port"
+    pool = ThreadPoolExecutor(max_workers=threads)
+
+    def all_cores(img):
+        # the reference's own _filter_rows over row blocks, then over column blocks
+        # (filtering.py:91-104 with every core instead of 4): bit-identical to serial
+        def one_pass(arr):
+            blocks = np.array_split(np.arange(arr.shape[0]), threads)
+            out = np.empty_like(arr)
+            for idx, res in zip(blocks, pool.map(lambda i: rows(arr[i]), blocks)):
+                out[idx] = res
+            return out
+
+        a = np.asarray(img, dtype=np.float64)
+        return one_pass(one_pass(a).T).T
+
+    return [("serial", 1, serial), ("parallel4", 4, par4), ("all_cores", threads, all_cores)], kind
+
+
+def _cpu_sample(cfg, px_target):
+    """A bounded sample of the config's workload: whole images (C3) or a full-width band."""
     from paper_1107_4958_b200 import synth, table_kernel
 
-    kern = table_kernel(cfg["k"], cfg["sigma"])
-    side_h, side_w = cfg["h"], cfg["w"]
+    pmax = table_kernel(cfg["k"], cfg["sigma"]).max_radius
     if cfg["dtype"] == "u8":
-        img = synth.to_u8(synth.one_over_f(side_h, side_w, 1000))
-    else:
-        # a sample band of the full-width image keeps the per-row cost of the real size
-        rows = int(max(2 * kern.max_radius + 2, min(side_h, sample_px_target // side_w)))
-        img = synth.one_over_f(rows, side_w, 42)
-    per_image = img.size
-    n_img = max(1, int(sample_px_target // per_image)) if cfg["dtype"] == "u8" else 1
-    channels = cfg["channels"]
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        for _i in range(n_img):
-            for _c in range(channels):
-                oracle.np_separable_filter_2d(img, kern.radii, kern.weights, threads=threads)
-        times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    px = n_img * per_image  # per-pixel metric counts each RGB pixel once (all channels)
-    desc = (f"{n_img} x {img.shape[0]}x{img.shape[1]} {cfg['dtype']} image(s) x {channels} channel(s), "
-            f"numpy port of filtering.py, {threads}-thread pool over row blocks, median of {reps}")
-    return px / t / 1e6, desc
+        imgs = [synth.to_u8(synth.one_over_f(cfg["h"], cfg["w"], 1000 + i))
+                for i in range(max(1, int(px_target // (cfg["h"] * cfg["w"]))))]
+        return imgs, f"{len(imgs)} x {cfg['h']}x{cfg['w']} u8 image(s) of the 256"
+    rows = int(min(cfg["h"], max(2 * pmax + 2, px_target // cfg["w"])))
+    img = synth.one_over_f(rows, cfg["w"], 42)
+    return [img] * cfg["channels"], f"{rows}x{cfg['w']} band of the image x {cfg['channels']} channel(s)"
+
+
+def cpu_reference(cfg, reps: int = 3, arms=("serial", "parallel4", "all_cores")):
+    """Medians of `reps` timings of each CPU arm on a bounded sample (Mpx/s)."""
+    fns, kind = _reference_arms(cfg)
+    big = cfg["h"] * cfg["w"] > 4096 * 4096
+    out = {}
+    for name, threads, fn in fns:
+        if name not in arms or (big and name != "all_cores"):
+            continue  # C4/C5: the serial arms need ~8 image copies of RAM (SURVEY §8(d))
+        target = (1 if name == "serial" else 4) * 1024 * 1024
+        imgs, desc = _cpu_sample(cfg, target)
+        fn(imgs[0][: min(imgs[0].shape[0], 256)])  # warm-up (page-in, thread pool)
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            for img in imgs:
+                fn(img)
+            times.append(time.perf_counter() - t0)
+        px = sum(im.size for im in imgs) / cfg["channels"]  # per-pixel metric counts an RGB pixel once
+        out[name] = {"value": round(px / statistics.median(times) / 1e6, 3), "threads": threads,
+                     "sample": desc, "reps": reps}
+    return out, kind
 
 
 def run_reference(args, cfg):
@@ -199,35 +296,41 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
-    sample = 4 * 1024 * 1024 if cfg["dtype"] == "u8" else 2 * 1024 * 1024
+    arms, kind = cpu_reference(cfg, reps=3)
+    fns, _ = _reference_arms(cfg)
+    fn = dict((n, f) for n, _, f in fns)["all_cores"]
+    imgs, desc = _cpu_sample(cfg, 4 * 1024 * 1024)
     for _ in range(args.warmup):
-        cpu_reference_rate(cfg, sample / 4, threads)
-    rates = []
+        fn(imgs[0][: min(imgs[0].shape[0], 256)])
+    times = []
     t0 = time.perf_counter()
-    desc = ""
     for _ in range(args.steps):
-        r, desc = cpu_reference_rate(cfg, sample, threads)
-        rates.append(r)
+        t1 = time.perf_counter()
+        for img in imgs:
+            fn(img)
+        times.append(time.perf_counter() - t1)
     elapsed = time.perf_counter() - t0
-    value = statistics.median(rates)
+    px = sum(im.size for im in imgs) / cfg["channels"]
+    value = px / statistics.median(times) / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * elapsed / max(1, args.steps), 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if args.config in ("c3", "c5") else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"]},
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{desc}; all-core row-block pool over the reference's _filter_rows, "
+                                   f"median of {args.steps} steps",
+                         "os_cpu_count": os.cpu_count(), "arms": arms},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def run_ours(args, cfg):
-    import ctypes
-
     import torch
     import torch.distributed as dist
 
-    from paper_1107_4958_b200 import _native as nat
     from paper_1107_4958_b200 import distributed as D
     from paper_1107_4958_b200 import filtering, table_kernel
 
@@ -239,44 +342,67 @@ def run_ours(args, cfg):
     kern = table_kernel(cfg["k"], cfg["sigma"])
     channels_last = cfg["channels"] > 1
     bound = 255.0
-    # config 5 on several GPUs: one image partitioned into row strips with a halo
-    # exchange; every other config: each rank filters its own batch (no collective)
+    # C5 on several GPUs: one image partitioned into row strips with a halo exchange;
+    # C3: BASELINE's 256 images sharded over the ranks; C1/C2/C4: one replica per rank
     strips = args.config == "c5" and world > 1
+    hs = None
     if strips:
-        full = make_inputs(cfg, 42, device)[0]  # same seed on every rank: identical image
         r0, r1 = D.shard_range(cfg["h"], rank, world)
-        x = full[r0:r1].contiguous()
+        full = make_inputs(cfg, 42, device)[0]  # same seed on every rank: identical image
+        hs = D.HaloStrip(r1 - r0, (cfg["w"],), kern.max_radius, torch.float32, device)
+        hs.interior.copy_(full[r0:r1])
         del full
+        x = hs.interior
         out = torch.empty(x.shape, dtype=torch.float32, device=device)
-        px_per_rank = (r1 - r0) * cfg["w"]
         px_total = cfg["h"] * cfg["w"]
         scaling = "strong"
-    else:
-        x = make_inputs(cfg, 1000 + rank * 100000 if cfg["dtype"] == "u8" else 42 + rank, device)
+        images = None
+    elif args.config == "c3":
+        i0, i1 = D.shard_range(cfg["batch"], rank, world)
+        x = make_inputs(cfg, 1000 + i0, device, count=i1 - i0)
         out = torch.empty(x.shape, dtype=torch.float32, device=device)
-        px_per_rank = cfg["batch"] * cfg["h"] * cfg["w"]
-        px_total = px_per_rank * world
+        px_total = cfg["batch"] * cfg["h"] * cfg["w"]
+        scaling = "strong"
+        images = (i0, i1)
+    else:
+        x = make_inputs(cfg, 42 + rank, device)
+        out = torch.empty(x.shape, dtype=torch.float32, device=device)
+        px_total = cfg["batch"] * cfg["h"] * cfg["w"] * world
         scaling = "weak"
+        images = None
     in_bytes = x.numel() * x.element_size()
     out_bytes = out.numel() * out.element_size()
     alg_bytes = in_bytes + out_bytes
 
-    lib = nat.load()
-    rp = np.ascontiguousarray(kern.radii, np.int64)
-    dcode = nat.SB_DTYPE_U8 if cfg["dtype"] == "u8" else nat.SB_DTYPE_F32
-    ws = lib.sb_separable_filter_2d_workspace_bytes(dcode, cfg["batch"], cfg["h"], cfg["w"], cfg["channels"],
-                                                    rp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), kern.k)
-    launches_per_step = 1 if ws == 0 else 2
     if strips:
         def step():
-            D.filter_strip(x, kern, channels_last=channels_last, value_bound=bound, out=out)
+            D.filter_strip(hs, kern, value_bound=bound, out=out, check=False)
     else:
         def step():
             filtering.separable_filter_batch(x, kern, channels_last=channels_last, value_bound=bound, out=out,
                                              check=False)
 
-    for _ in range(args.warmup):
+    for _ in range(max(2, args.warmup)):
         step()
+    torch.cuda.synchronize()
+    kernels = count_kernels(step)
+    # one CUDA graph of the public call per step (launch overhead off the critical path of
+    # small per-GPU shards); the strip path keeps NCCL outside graphs
+    graph = None
+    if not strips and not args.no_graph:
+        s_cap = torch.cuda.Stream()
+        s_cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_cap):
+            step()
+        torch.cuda.current_stream().wait_stream(s_cap)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        timed = graph.replay
+    else:
+        timed = step
+    for _ in range(args.warmup):
+        timed()
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local)
@@ -288,7 +414,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(args.steps):
-        step()
+        timed()
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -297,26 +423,40 @@ def run_ours(args, cfg):
     # keep the GPU loaded ~1 s more (untimed) so the clock sampler sees the load
     t_end = time.time() + max(0.0, 1.2 - ms / 1e3)
     while time.time() < t_end:
-        step()
+        timed()
         torch.cuda.synchronize()
     clocks = sampler.stop()
     ms_max = D.max_over_ranks(ms, device=device)
     ms_per_step = ms_max / args.steps
     value = px_total * args.steps / (ms_max / 1e3) / 1e6
 
-    # e2e through the public API from pinned host memory (H2D of the inputs and
-    # D2H of the filtered images inside the timed region)
+    # e2e through the public API from pinned host memory (H2D of the inputs and D2H of
+    # the filtered images inside the timed region)
     x_host = x.cpu().pin_memory()
     out_host = torch.empty(out.shape, dtype=torch.float32).pin_memory()
     if strips:
+        e2e_api = "distributed.filter_strip (no value_bound) from/to pinned host strips"
+
         def e2e_step():
-            res = D.filter_strip(x_host.to(device, non_blocking=True), kern, channels_last=channels_last,
-                                 value_bound=bound, out=out)
+            hs.interior.copy_(x_host, non_blocking=True)
+            res = D.filter_strip(hs, kern, out=out)
             out_host.copy_(res)
-    else:
+    elif args.config == "c3":
+        e2e_api = "separable_filter_batch(pinned host uint8 batch, kern, out=pinned host)"
+
         def e2e_step():
-            filtering.separable_filter_batch(x_host, kern, channels_last=channels_last, value_bound=bound,
-                                             out=out_host, check=False)
+            filtering.separable_filter_batch(x_host, kern, out=out_host)
+    elif not channels_last:
+        e2e_api = "separable_filter_2d(pinned host image, kern, out=pinned host) - reference signature, no value_bound"
+
+        def e2e_step():
+            filtering.separable_filter_2d(x_host[0], kern, out=out_host[0])
+    else:
+        e2e_api = "separable_filter_batch(pinned host HxWx3, kern, channels_last=True, out=pinned host), no value_bound"
+
+        def e2e_step():
+            filtering.separable_filter_batch(x_host, kern, channels_last=True, out=out_host)
+    e2e_step()
     e2e_step()
     torch.cuda.synchronize()
     if world > 1:
@@ -334,8 +474,10 @@ def run_ours(args, cfg):
 
     threads = len(os.sched_getaffinity(0))
     if strips:
-        max_abs = rmse = None  # checked by tests/test_gpu_parity.py::test_row_window_strips_match_full_image
+        max_abs = rmse = None  # tests/test_gpu_domain.py::test_overlapped_strips_match_full_image
     else:
+        step()
+        torch.cuda.synchronize()
         xs = x[0].cpu().numpy()
         got = out[0].cpu().numpy()
         if channels_last:
@@ -368,34 +510,40 @@ def run_ours(args, cfg):
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        rate, desc = cpu_reference_rate(cfg, 4 * 1024 * 1024 if cfg["dtype"] == "u8" else 2 * 1024 * 1024, threads)
-        cpu = {"value": round(rate, 3), "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+        arms, kind = cpu_reference(cfg, reps=3)
+        a = arms["all_cores"]
+        cpu = {"value": a["value"], "unit": UNIT, "cores": a["threads"], "kind": kind,
+               "sample": a["sample"] + "; all-core row-block pool over the reference's _filter_rows (bit-identical "
+                                       "to its serial call), median of 3", "os_cpu_count": os.cpu_count(),
+               "arms": arms}
     peak, peak_kind = _peaks()
     # algorithmic bytes of a step (one read of every input pixel, one write of every output
-    # pixel) over the CUDA-event step time; for the two-launch path the pair is the unit
+    # pixel) over the CUDA-event step time (max over ranks)
     achieved = alg_bytes / (ms_per_step / 1e3) / 1e9
     traffic = _traffic_from_profiles(args.config)
+    n_launch = len(kernels) if kernels is not None else None
+    kinds = sorted({k.split("<")[0].split("(")[0] for k in kernels}) if kernels else None
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "source_dtype": cfg["dtype"], "output_dtype": "f32",
-                   "per_gpu_images": cfg["batch"] if not strips else None,
-                   "global_images": cfg["batch"] * world if not strips else 1,
+                   "images_rank0": list(images) if images else None,
+                   "global_images": cfg["batch"] if args.config == "c3" else (1 if strips else world),
                    "height": cfg["h"], "width": cfg["w"], "channels": cfg["channels"], "k": cfg["k"],
                    "sigma": cfg["sigma"], "radii": kern.radii.tolist(),
-                   "parallelism": (f"row strips x{world} + NCCL halo exchange" if strips
-                                   else f"dp{world} (image batch sharded, no collective)"),
-                   "l2": ("inputs+outputs per step exceed the 126 MB L2; no flush" if alg_bytes > 2 * 126e6 else
+                   "parallelism": (f"row strips x{world} + NCCL halo exchange" if strips else
+                                   f"dp{world} (BASELINE's 256 images sharded, no collective)" if args.config == "c3"
+                                   else f"{world} replica(s)"),
+                   "timed_call": "CUDA graph replay of separable_filter_batch" if graph is not None else "eager",
+                   "l2": ("inputs+outputs per rank exceed the 126 MB L2; no flush" if alg_bytes > 2 * 126e6 else
                           "working set fits the 126 MB L2 (parity-size config)")},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "algorithmic_bytes_per_step": alg_bytes,
-                     "kernel": "fused_kernel (one launch per step)" if ws == 0 else
-                               "stream_rows_kernel + cols2_kernel (two launches per step, timed together)"},
+                     "algorithmic_bytes_per_step": alg_bytes, "kernels_per_step": kinds},
         "e2e": {"value": round(e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(in_bytes),
-                "d2h_bytes_per_step": int(out_bytes)},
-        "gpu_launches": int(args.steps * launches_per_step),
+                "d2h_bytes_per_step": int(out_bytes), "api": e2e_api},
+        "gpu_launches": int(args.steps * n_launch) if n_launch is not None else None,
         "parity": {"max_abs": max_abs, "rmse": rmse, "scope": "rank-0 image 0 vs C oracle"},
         "quality": quality,
         "clocks": clocks,
@@ -407,6 +555,32 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def launch_check():
+    """Rank-side check of the self-launch (tests/test_bench_cpu.py): gloo all-reduce."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, _ = _dist()
+    dist.init_process_group("gloo")
+    t = torch.tensor([rank + 1])
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "world": world, "rank_sum": int(t.item())}), flush=True)
+    dist.destroy_process_group()
+
+
+def relaunch(args_list, n):
+    """Re-run this script as n torchrun ranks (one per GPU) and return its exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *args_list]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -415,7 +589,14 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager calls instead of a CUDA graph replay")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(sys.argv[1:], args.gpus))
+    if args.launch_check:
+        launch_check()
+        return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -48,7 +48,20 @@
 extern "C" {
 #endif
 
-#define SB_MAX_K 8
+/* Largest k (number of slices) the library accepts.  The templated sweep
+ * kernels take k <= 8 (the paper's kernels have k = 3..5); larger k runs the
+ * generic two-pass kernels, which also cover every radius < extent. */
+#define SB_MAX_K 1024
+
+/* Path policy (sb_set_path_policy): AUTO picks the fastest path that applies;
+ * the others force a path for A/B timing and for the bit-identity tests. */
+enum {
+  SB_PATH_AUTO = 0,
+  SB_PATH_GENERIC = 1,      /* generic two-pass kernels (row prefix, column prefix) for every call */
+  SB_PATH_UNFUSED = 2,      /* row pass to an int32 plane, then a column kernel (no fused sweep)     */
+  SB_PATH_U8_THREE_CTA = 3, /* uint8 fused sweep: three CTAs per SM, one band per consumer turn     */
+  SB_PATH_U8_ONE_BAND = 4   /* uint8 fused sweep: two CTAs per SM, one band per consumer turn       */
+};
 
 /* return codes */
 enum {
@@ -64,10 +77,19 @@ enum {
 enum { SB_DTYPE_U8 = 0, SB_DTYPE_U16 = 1, SB_DTYPE_F32 = 2, SB_DTYPE_F64 = 3 };
 
 /* bits written (atomicOr) into *status_dev by the kernels */
-#define SB_STATUS_RANGE 1 /* a pixel exceeded value_bound (or was NaN/Inf) */
+#define SB_STATUS_RANGE 1 /* a pixel exceeded value_bound (or was NaN/Inf)                     */
+#define SB_STATUS_HALF 2  /* float sources: some |pixel| >= value_bound / 2.  A caller that     \
+                             guessed the bound (e.g. from its previous image) keeps the result \
+                             when RANGE is clear and HALF is set: the quantum is then within   \
+                             one bit of the one the measured maximum gives.                    */
 
 /* ABI version, bumped on any signature change. */
 int sb_version(void);
+
+/* Thread-local path policy (SB_PATH_*) for the calls made afterwards on this
+ * thread; returns the previous policy, or -1 for an unknown value.  The
+ * workspace queries honour it too. */
+int sb_set_path_policy(int policy);
 
 /* Thread-local description of the last error returned on this thread. */
 const char* sb_last_error(void);
@@ -110,14 +132,19 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
                                   void* stream);
 
 /* filtering.py:48-64 _filter_rows: the row pass alone, every row of a
- * (rows x width) array (row stride in elements), float32 output. */
+ * (rows x width) array (row stride in elements), float32 output.  Needs
+ * sb_filter_rows_workspace_bytes(...) bytes of workspace (0 unless the row is
+ * too long for the shared-memory prefix of the generic kernel). */
+size_t sb_filter_rows_workspace_bytes(int src_dtype, int64_t rows, int64_t width, const int64_t* radii, int k);
 int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, int64_t src_row_stride,
                    float* dst, int64_t dst_row_stride, const int64_t* radii, const double* weights, int k,
-                   double value_bound, int* status_dev, void* stream);
+                   double value_bound, void* workspace, size_t workspace_bytes, int* status_dev, void* stream);
 
-/* filtering.py:67-73 slice_filter_1d on one signal of length n. */
+/* filtering.py:67-73 slice_filter_1d on one signal of length n (workspace as
+ * sb_filter_rows with rows = 1, width = n). */
 int sb_slice_filter_1d(const void* src, int src_dtype, int64_t n, float* dst, const int64_t* radii,
-                       const double* weights, int k, double value_bound, int* status_dev, void* stream);
+                       const double* weights, int k, double value_bound, void* workspace, size_t workspace_bytes,
+                       int* status_dev, void* stream);
 
 /* filtering.py:31-36 prefix_sum: inclusive float64 scan of n >= 1 values.
  * Needs sb_prefix_sum_workspace_bytes(n) bytes of device workspace. */

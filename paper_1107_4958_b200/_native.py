@@ -26,16 +26,26 @@ SB_DTYPE_F32 = 2
 SB_DTYPE_F64 = 3
 
 SB_STATUS_RANGE = 1
-SB_MAX_K = 8
+SB_STATUS_HALF = 2
+SB_MAX_K = 1024  # the templated sweep kernels take k <= 8; larger k runs the generic kernels
+ABI_VERSION = 4
+
+SB_PATH_AUTO = 0
+SB_PATH_GENERIC = 1
+SB_PATH_UNFUSED = 2
+SB_PATH_U8_THREE_CTA = 3
+SB_PATH_U8_ONE_BAND = 4
 
 #: Every symbol include/sliceblur_b200.h declares (tests check the exports).
 EXPORTED_SYMBOLS = (
     "sb_version",
+    "sb_set_path_policy",
     "sb_last_error",
     "sb_check_kernel",
     "sb_separable_filter_2d_workspace_bytes",
     "sb_separable_filter_2d",
     "sb_separable_filter_2d_window",
+    "sb_filter_rows_workspace_bytes",
     "sb_filter_rows",
     "sb_slice_filter_1d",
     "sb_prefix_sum_workspace_bytes",
@@ -66,6 +76,8 @@ _size = ctypes.c_size_t
 def _declare(lib):
     lib.sb_version.argtypes = []
     lib.sb_version.restype = _int
+    lib.sb_set_path_policy.argtypes = [_int]
+    lib.sb_set_path_policy.restype = _int
     lib.sb_last_error.argtypes = []
     lib.sb_last_error.restype = ctypes.c_char_p
     lib.sb_check_kernel.argtypes = [_i64p, _f64p, _int, _i64]
@@ -87,10 +99,13 @@ def _declare(lib):
         _vp, _size, _vp, _vp,
     ]
     lib.sb_separable_filter_2d_window.restype = _int
-    lib.sb_filter_rows.argtypes = [_vp, _int, _i64, _i64, _i64, _vp, _i64, _i64p, _f64p, _int, ctypes.c_double, _vp,
-                                   _vp]
+    lib.sb_filter_rows_workspace_bytes.argtypes = [_int, _i64, _i64, _i64p, _int]
+    lib.sb_filter_rows_workspace_bytes.restype = _size
+    lib.sb_filter_rows.argtypes = [_vp, _int, _i64, _i64, _i64, _vp, _i64, _i64p, _f64p, _int, ctypes.c_double,
+                                   _vp, _size, _vp, _vp]
     lib.sb_filter_rows.restype = _int
-    lib.sb_slice_filter_1d.argtypes = [_vp, _int, _i64, _vp, _i64p, _f64p, _int, ctypes.c_double, _vp, _vp]
+    lib.sb_slice_filter_1d.argtypes = [_vp, _int, _i64, _vp, _i64p, _f64p, _int, ctypes.c_double, _vp, _size, _vp,
+                                       _vp]
     lib.sb_slice_filter_1d.restype = _int
     lib.sb_prefix_sum_workspace_bytes.argtypes = [_i64]
     lib.sb_prefix_sum_workspace_bytes.restype = _size
@@ -125,6 +140,8 @@ def load():
         except OSError as exc:  # pragma: no cover - depends on the host
             raise NativeLibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
         _declare(lib)
+        if lib.sb_version() != ABI_VERSION:
+            raise NativeLibraryError(f"{LIB_PATH} has ABI {lib.sb_version()}, this package needs {ABI_VERSION}; rebuild")
         _lib = lib
     return _lib
 
@@ -132,3 +149,26 @@ def load():
 def last_error() -> str:
     msg = load().sb_last_error()
     return msg.decode("utf-8", "replace") if msg else ""
+
+
+class path_policy:
+    """Context manager forcing a path (SB_PATH_*) for the calls made on this thread.
+
+    ``with path_policy(SB_PATH_GENERIC): ...`` runs the generic two-pass kernels; the
+    tests use it to prove that every path gives bit-identical results.
+    """
+
+    def __init__(self, policy: int):
+        self.policy = policy
+        self.prev = None
+
+    def __enter__(self):
+        prev = load().sb_set_path_policy(self.policy)
+        if prev < 0:
+            raise ValueError(f"unknown path policy {self.policy}")
+        self.prev = prev
+        return self
+
+    def __exit__(self, *exc):
+        load().sb_set_path_policy(self.prev)
+        return False

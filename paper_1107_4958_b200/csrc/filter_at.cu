@@ -10,66 +10,63 @@
 
 namespace sb {
 
-// R[col][y]: the row value at (y, cols[col]) rounded to the mid quantum; the k box
-// sums come from one walk over the 2*pmax+1 taps (replicate boundary, nested boxes).
+// R[col][y]: the row value at (y, cols[col]) rounded to the mid quantum.  The k nested
+// boxes grow outward from the pixel (replicate boundary): box i adds the taps
+// p_{i-1} < |d| <= p_i to box i-1, and is weighted as soon as it is complete, so the
+// fp32 sum runs in slice order like every other kernel's.
 template <typename Tin>
 __global__ void __launch_bounds__(128) filter_at_rows_kernel(const Tin* __restrict__ src, long long row_stride, int H,
                                                              int W, const int* __restrict__ cols, int* __restrict__ R,
-                                                             Taps t, int* status) {
+                                                             const __grid_constant__ TapsG t, int* status) {
   const int y = blockIdx.x * blockDim.x + threadIdx.x;
   const int ci = blockIdx.y;
   if (y >= H) return;
   const int x = cols[ci];
   const Tin* row = src + (long long)y * row_stride;
-  int box[SB_MAX_K];
-#pragma unroll
-  for (int i = 0; i < SB_MAX_K; ++i) box[i] = 0;
-  bool bad = false;
-  for (int d = -t.pmax; d <= t.pmax; ++d) {
-    const int v = to_fixed<Tin>(row[min(max(x + d, 0), W - 1)], t, bad);
-    const int ad = d < 0 ? -d : d;
-#pragma unroll
-    for (int i = 0; i < SB_MAX_K; ++i)
-      if (i < t.k && ad <= t.p[i]) box[i] += v;
-  }
+  uint32_t bad = 0;
+  long long box = 0;  // int64: exact for the int32 quanta and for the wide (int64) ones alike
+  int covered = -1;
   float acc = 0.0f;
-#pragma unroll
-  for (int i = 0; i < SB_MAX_K; ++i)
-    if (i < t.k) acc = fmaf(t.w_row[i], i2f_fast((uint32_t)box[i]), acc);
+  for (int i = 0; i < t.k; ++i) {
+    for (int d = covered + 1; d <= t.p[i]; ++d) {
+      box += to_fixed<Tin>(row[min(x + d, W - 1)], t, bad);
+      if (d > 0) box += to_fixed<Tin>(row[max(x - d, 0)], t, bad);
+    }
+    covered = t.p[i];
+    acc = fmaf(t.w_row[i], __ll2float_rn(box), acc);
+  }
   R[(long long)ci * H + y] = __float_as_int(acc + kMagic) - kMagicBits;
-  if (bad && status) atomicOr(status, SB_STATUS_RANGE);
+  report_status(status, bad);
 }
 
 // out[n]: the column pass of column pt_col[n] at row pt_y[n] (exact wrapping int32
-// box sums of R, weighted in fp32 in box order as the sweeps do)
+// box sums of R, weighted in fp32 in slice order as the sweeps do)
 __global__ void __launch_bounds__(128) filter_at_points_kernel(const int* __restrict__ R, int H,
                                                                const int* __restrict__ pt_col,
                                                                const int* __restrict__ pt_y, long long npts,
-                                                               float* __restrict__ out, Taps t) {
+                                                               float* __restrict__ out,
+                                                               const __grid_constant__ TapsG t) {
   const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= npts) return;
   const int* rc = R + (long long)pt_col[n] * H;
   const int y = pt_y[n];
-  uint32_t box[SB_MAX_K];
-#pragma unroll
-  for (int i = 0; i < SB_MAX_K; ++i) box[i] = 0;
-  for (int d = -t.pmax; d <= t.pmax; ++d) {
-    const uint32_t v = (uint32_t)rc[min(max(y + d, 0), H - 1)];
-    const int ad = d < 0 ? -d : d;
-#pragma unroll
-    for (int i = 0; i < SB_MAX_K; ++i)
-      if (i < t.k && ad <= t.p[i]) box[i] += v;
-  }
+  long long box = 0;
+  int covered = -1;
   float acc = 0.0f;
-#pragma unroll
-  for (int i = 0; i < SB_MAX_K; ++i)
-    if (i < t.k) acc = fmaf(t.w_col[i], i2f_fast(box[i]), acc);
+  for (int i = 0; i < t.k; ++i) {
+    for (int d = covered + 1; d <= t.p[i]; ++d) {
+      box += rc[min(y + d, H - 1)];
+      if (d > 0) box += rc[max(y - d, 0)];
+    }
+    covered = t.p[i];
+    acc = fmaf(t.w_col[i], __ll2float_rn(box), acc);
+  }
   out[n] = acc;
 }
 
 int launch_filter_at(const void* src, int src_dtype, long long row_stride, int H, int W, const int* cols, int ncols,
-                     const int* pt_col, const int* pt_y, long long npts, float* out, int* R, const Taps& t, int* status,
-                     cudaStream_t st) {
+                     const int* pt_col, const int* pt_y, long long npts, float* out, int* R, const TapsG& t,
+                     int* status, cudaStream_t st) {
   const dim3 g1((H + 127) / 128, ncols);
   switch (src_dtype) {
     case SB_DTYPE_U8:

@@ -23,6 +23,13 @@
 namespace {
 
 thread_local std::string g_last_error;
+thread_local int g_policy = SB_PATH_AUTO;  // sb_set_path_policy
+
+// SB_DEBUG=1 prints the launch plans to stderr (read once, not per call)
+bool debug_plans() {
+  static const bool on = std::getenv("SB_DEBUG") != nullptr;
+  return on;
+}
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -60,11 +67,15 @@ int quantum_exponent(double bound, double limit) {
 }
 
 struct Plan {
-  sb::Taps taps;
+  sb::Taps taps;  // k <= FAST_K (templated sweep kernels)
+  sb::TapsG tg;   // any k (generic kernels, filter_at); only the first k entries are set
   int pmax;
 };
 
-int make_taps(const int64_t* radii, const double* weights, int k, int src_dtype, double value_bound, Plan* plan) {
+// Fixed-point quanta.  `wide`: the generic kernels' int64 box sums
+// (2*pmax+1 > kWideSpan), so only the magic-number rounding bounds the quanta.
+int make_taps(const int64_t* radii, const double* weights, int k, int src_dtype, double value_bound, Plan* plan,
+              bool wide = false) {
   int rc = validate_kernel(radii, weights, k);
   if (rc) return rc;
   double bound;
@@ -80,12 +91,21 @@ int make_taps(const int64_t* radii, const double* weights, int k, int src_dtype,
       if (!(value_bound >= 0.0) || !std::isfinite(value_bound))
         return fail(SB_ERR_INVALID_ARGUMENT, "float input needs a finite value_bound >= 0 (max |pixel|)");
       bound = value_bound;
+      if (bound < 3.0e38) {
+        // the kernels quantise (float)v: a double just below the bound can round up to the
+        // float above it, so the quantum must admit the bound rounded up to float (a float32
+        // pixel <= bound is <= it too)
+        float bf = (float)bound;
+        if ((double)bf < bound) bf = std::nextafter(bf, INFINITY);
+        bound = (double)bf;
+      }
       break;
     default: return fail(SB_ERR_INVALID_ARGUMENT, "unknown src_dtype");
   }
   const int pmax = (int)radii[k - 1];
   const double width = 2.0 * pmax + 1.0;
-  const double box_limit = 2147483647.0 - 2.0 * width;  // |box sum| < 2^31 incl. rounding
+  // |box sum| < 2^31 (int32) or 2^62 (wide) incl. rounding
+  const double box_limit = wide ? 4.6e18 : 2147483647.0 - 2.0 * width;
   int s_in = 0;
   if (src_dtype == SB_DTYPE_F32 || src_dtype == SB_DTYPE_F64) {
     s_in = std::min(quantum_exponent(bound, 4194304.0), quantum_exponent(width * bound, box_limit));
@@ -98,18 +118,39 @@ int make_taps(const int64_t* radii, const double* weights, int k, int src_dtype,
   const double rbound = gabs * (bound + std::ldexp(0.5, -s_in)) * (1.0 + 1e-6);
   const int s_mid = std::min(quantum_exponent(rbound, 4194304.0), quantum_exponent(width * rbound, box_limit));
 
+  sb::TapsG& g = plan->tg;
+  g.k = k;
+  g.pmax = pmax;
+  g.in_scale = (float)std::ldexp(1.0, s_in);
+  if (src_dtype == SB_DTYPE_F32 || src_dtype == SB_DTYPE_F64) {
+    // |pixel| * 2^s_in <= the scaled bound (< 2^22, exact: bound is a float here), so every
+    // sum the quanta were sized for stays in range; half of it flags SB_STATUS_HALF
+    const float bf = (float)bound;
+    g.in_limit = (float)std::ldexp((double)bf, s_in);
+    g.seen_limit = (float)std::ldexp((double)bf, s_in - 1);
+  } else {
+    g.in_limit = (float)bound;  // uint16: largest admissible sample (uint8: unused)
+    g.seen_limit = INFINITY;
+  }
+  for (int i = 0; i < k; ++i) {
+    g.p[i] = (int)radii[i];
+    g.w_row[i] = (float)std::ldexp(weights[i], s_mid - s_in);
+    g.w_col[i] = (float)std::ldexp(weights[i], -s_mid);
+    g.w_out1[i] = (float)std::ldexp(weights[i], -s_in);
+  }
   sb::Taps& t = plan->taps;
   std::memset(&t, 0, sizeof(t));
   t.k = k;
   t.pmax = pmax;
-  for (int i = 0; i < k; ++i) {
-    t.p[i] = (int)radii[i];
-    t.w_row[i] = (float)std::ldexp(weights[i], s_mid - s_in);
-    t.w_col[i] = (float)std::ldexp(weights[i], -s_mid);
-    t.w_out1[i] = (float)std::ldexp(weights[i], -s_in);
+  for (int i = 0; i < k && i < sb::FAST_K; ++i) {
+    t.p[i] = g.p[i];
+    t.w_row[i] = g.w_row[i];
+    t.w_col[i] = g.w_col[i];
+    t.w_out1[i] = g.w_out1[i];
   }
-  t.in_scale = (float)std::ldexp(1.0, s_in);
-  t.in_limit = src_dtype == SB_DTYPE_U16 ? (float)bound : 4194304.0f;  // uint16: largest admissible sample
+  t.in_scale = g.in_scale;
+  t.in_limit = g.in_limit;
+  t.seen_limit = g.seen_limit;
   plan->pmax = pmax;
   return SB_OK;
 }
@@ -184,15 +225,14 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
     // SB_FUSED=3: fused_kernel<uint8_t, K, 3>, three CTAs per SM (registers rebalanced between
     // the producer and consumer warpgroups with setmaxnreg, single-buffered staging and output
     // box).  SB_FUSED=1: the two-CTA one-band kernel.  (A/B switches.)
-    const char* fe = std::getenv("SB_FUSED");
-    if (!fe || std::atoi(fe) == 5) {
+    if (g_policy != SB_PATH_U8_THREE_CTA && g_policy != SB_PATH_U8_ONE_BAND) {
       // two bands per consumer iteration: 32-row ring slots, 32-row mirror
       tl.split = 5;
       tl.D = ((2 * pmax + 65 + 31) / 32) * 32;
       int cols5 = 32;
       while (cols5 < tl.D + 32) cols5 <<= 1;
       tl.tmem_cols = cols5;
-    } else if (std::atoi(fe) == 3) {
+    } else if (g_policy == SB_PATH_U8_THREE_CTA) {
       tl.split = 3;
       const size_t end = (size_t)sb::FPROD * sb::HB * tl.stage_row_bytes +
                          (size_t)sb::FPROD * (sb::HB / 2) * sb::LSP2 * sizeof(float2);
@@ -393,7 +433,7 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, in
   tl.rows_per_item = rows_per_item;
   if (columns * items > 0x7fffffffLL) return fail(SB_ERR_INVALID_ARGUMENT, "image too large for the grid");
   out->grid = dim3((unsigned)(tl.nstrips * items), (unsigned)channels, 1);
-  if (std::getenv("SB_DEBUG"))
+  if (debug_plans())
     std::fprintf(stderr,
                  "[sliceblur_b200] mode=%d pmax=%d L=%d ls=%d D=%d tmem_cols=%d packed=%d smem=%zu occ=%d "
                  "strips=%d items=%lld rows/item=%lld grid=%u x %u\n",
@@ -480,11 +520,98 @@ int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, c
   return SB_OK;
 }
 
+// ---------------------------------------------------------------- path choice
+// One decision shared by the workspace queries and the launches (so a caller that
+// sized its workspace with the query always has enough).
+enum class RowPath { Fused, Stream, Tiled, Generic };
+enum class ColPath { None, Prefix, Running, Generic };
+
+struct Route {
+  RowPath rows;
+  ColPath cols;
+  bool wide;             // generic kernels with int64 sums and an int64 plane
+  size_t scratch_bytes;  // generic row kernel's global scratch rows
+};
+
+bool needs_wide(int pmax) { return 2LL * pmax + 1 > sb::kWideSpan; }
+
+size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+bool stream_rows_fits(int src_dtype, int pmax) {
+  const int xs = -(((pmax + 1) + 15) & ~15);
+  const int lagc = (sb::CW - 1 - xs + pmax) / sb::CW;
+  return src_dtype == SB_DTYPE_F32 && lagc + 1 < sb::NSLOT;
+}
+
+bool tiled_rows_fits(sb::Mode m, int pmax, int channels, int es) {
+  const sb::Tiling tl = make_tiling(m, pmax, channels, es, false);
+  return smem_bytes(tl, m) <= 227 * 1024;
+}
+
+// The running-sum column kernel reads every lead window from its TMEM ring: the ring
+// (capped at 496 rows) must span pmax - p_0 + 2 bands (see cols_kernel).
+bool running_cols_fits(const int64_t* radii, int pmax, int channels) {
+  const sb::Tiling ct = make_tiling(sb::Mode::ColsFromMid, pmax, channels, 4, false);
+  return ct.D >= pmax - (int)radii[0] + 2 * sb::HB;
+}
+
+Route route_2d(int src_dtype, int64_t width, int channels, const int64_t* radii, int k) {
+  const int pmax = (int)radii[k - 1];
+  Route r{RowPath::Generic, ColPath::Generic, needs_wide(pmax), 0};
+  const int es = dtype_size(src_dtype);
+  const bool fast = k <= sb::FAST_K && g_policy != SB_PATH_GENERIC && !r.wide;
+  if (fast && g_policy != SB_PATH_UNFUSED && fused_fits(pmax, channels, es)) {
+    r.rows = RowPath::Fused;
+    r.cols = ColPath::None;
+    return r;
+  }
+  if (fast) {
+    if (stream_rows_fits(src_dtype, pmax))
+      r.rows = RowPath::Stream;
+    else if (tiled_rows_fits(sb::Mode::RowsToMid, pmax, channels, es))
+      r.rows = RowPath::Tiled;
+    sb::Tiling ct = make_tiling(sb::Mode::ColsFromMid, pmax, channels, 4, false), pt;
+    if (cols_prefix_tiling(ct, radii, k, pmax, &pt))
+      r.cols = ColPath::Prefix;
+    else if (running_cols_fits(radii, pmax, channels))
+      r.cols = ColPath::Running;
+  }
+  if (r.rows == RowPath::Generic) r.scratch_bytes = sb::generic_rows_scratch_bytes((int)width, r.wide);
+  return r;
+}
+
+RowPath route_rows_only(int src_dtype, int64_t width, int k, int pmax) {
+  if (k <= sb::FAST_K && g_policy != SB_PATH_GENERIC && !needs_wide(pmax) &&
+      tiled_rows_fits(sb::Mode::RowsToOut, pmax, 1, dtype_size(src_dtype)))
+    return RowPath::Tiled;
+  (void)width;
+  return RowPath::Generic;
+}
+
+int device_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  static int cache[64] = {0};
+  if (!cache[dev]) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = sms;
+  }
+  return cache[dev];
+}
+
 }  // namespace
 
 extern "C" {
 
-int sb_version(void) { return 3; }
+int sb_version(void) { return 4; }
+
+int sb_set_path_policy(int policy) {
+  if (policy < SB_PATH_AUTO || policy > SB_PATH_U8_ONE_BAND) return -1;
+  const int prev = g_policy;
+  g_policy = policy;
+  return prev;
+}
 
 size_t sb_filter_at_workspace_bytes(int64_t height, int64_t ncols) {
   if (height < 1 || ncols < 1) return 0;
@@ -504,14 +631,15 @@ int sb_filter_at(const void* src, int src_dtype, int64_t height, int64_t width, 
   if (rc) return rc;
   rc = sb_check_kernel(radii, weights, k, height);
   if (rc) return rc;
-  Plan plan;
-  rc = make_taps(radii, weights, k, src_dtype, value_bound, &plan);
+  static thread_local Plan plan;  // 16 KB of generic taps: not on the stack of every call
+  // the same quanta as the full filter of this image (sb_separable_filter_2d): wide past kWideSpan
+  rc = make_taps(radii, weights, k, src_dtype, value_bound, &plan, needs_wide((int)radii[k - 1]));
   if (rc) return rc;
   const size_t need = sb_filter_at_workspace_bytes(height, ncols);
   if (!workspace || workspace_bytes < need)
     return fail(SB_ERR_WORKSPACE, "workspace of " + std::to_string(need) + " bytes required");
   const int e = sb::launch_filter_at(src, src_dtype, src_row_stride, (int)height, (int)width, cols, (int)ncols,
-                                     pt_col, pt_y, npts, out, (int*)workspace, plan.taps, status_dev,
+                                     pt_col, pt_y, npts, out, (int*)workspace, plan.tg, status_dev,
                                      (cudaStream_t)stream);
   if (e) return cuda_fail((cudaError_t)e, "filter_at launch");
   return SB_OK;
@@ -534,10 +662,11 @@ int sb_check_kernel(const int64_t* radii, const double* weights, int k, int64_t 
 size_t sb_separable_filter_2d_workspace_bytes(int src_dtype, int64_t batch, int64_t height, int64_t width,
                                               int channels, const int64_t* radii, int k) {
   if (!radii || k < 1 || k > SB_MAX_K || batch < 1 || height < 1 || width < 1 || channels < 1) return 0;
-  const int es = dtype_size(src_dtype);
-  if (es == 0) return 0;
-  if (fused_fits((int)radii[k - 1], channels, es)) return 0;
-  return (size_t)batch * height * width * channels * sizeof(int);
+  if (dtype_size(src_dtype) == 0 || radii[k - 1] < 0 || radii[k - 1] > 0x7fffffff) return 0;
+  const Route r = route_2d(src_dtype, width, channels, radii, k);
+  if (r.rows == RowPath::Fused) return 0;
+  const size_t plane = (size_t)batch * height * width * channels * (r.wide ? sizeof(long long) : sizeof(int));
+  return r.scratch_bytes ? align256(plane) + r.scratch_bytes : plane;
 }
 
 int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch, int64_t height, int64_t width,
@@ -561,8 +690,9 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
   if (rc) return rc;
   rc = sb_check_kernel(radii, weights, k, height);
   if (rc) return rc;
-  Plan plan;
-  rc = make_taps(radii, weights, k, src_dtype, value_bound, &plan);
+  const Route route = route_2d(src_dtype, width, channels, radii, k);
+  static thread_local Plan plan;
+  rc = make_taps(radii, weights, k, src_dtype, value_bound, &plan, route.wide);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
 
@@ -586,11 +716,9 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
                (batch == 1 || (dst_image_stride * 4) % 16 == 0);
   const long long total_rows = (long long)batch * (row_end - row_begin);  // rows the column sweep outputs
   const long long all_rows = (long long)batch * height;                   // rows the row pass produces
-  const bool u8_single = (src_dtype == SB_DTYPE_U8 && channels == 1);
-  const sb::Tiling base = make_tiling(sb::Mode::Fused, plan.pmax, channels, g.es, u8_single);
-
-  const size_t need = sb_separable_filter_2d_workspace_bytes(src_dtype, batch, height, width, channels, radii, k);
-  if (need == 0) {
+  if (route.rows == RowPath::Fused) {
+    const bool u8_single = (src_dtype == SB_DTYPE_U8 && channels == 1);
+    const sb::Tiling base = make_tiling(sb::Mode::Fused, plan.pmax, channels, g.es, u8_single);
     const void* fn = base.split == 3   ? sb::sweep_ptr_fused3(k)
                      : base.split == 5 ? sb::sweep_ptr_fused5(k)
                                        : pick_kernel(sb::Mode::Fused, src_dtype, k);
@@ -599,80 +727,102 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     if (rc) return rc;
     return launch_fused(fn, L, src, dst, g, plan.taps, status_dev, st);
   }
-  // two launches through an int32 workspace laid out [channel][batch][H][W]
+  // two passes through an int32 workspace laid out [channel][batch][H][W]
+  const size_t need = sb_separable_filter_2d_workspace_bytes(src_dtype, batch, height, width, channels, radii, k);
   if (!workspace || workspace_bytes < need)
     return fail(SB_ERR_WORKSPACE, "workspace of " + std::to_string(need) + " bytes required");
   int* mid = (int*)workspace;
   g.mid_row = width;
   g.mid_img = (long long)height * width;
   g.mid_ch = g.mid_img * batch;
-  // streaming row pass (full-width bands, prefix carried across chunks) when it applies
-  const int xs = -(((plan.pmax + 1) + 15) & ~15);  // first halo column, 16-aligned
-  const int lagc = (sb::CW - 1 - xs + plan.pmax) / sb::CW;
-  if (src_dtype == SB_DTYPE_F32 && lagc + 1 < sb::NSLOT) {
+  const int sms = device_sms();
+
+  // ---- row pass
+  if (route.rows == RowPath::Stream) {
+    // streaming row pass: full-width bands, prefix carried across chunks
+    const int xs = -(((plan.pmax + 1) + 15) & ~15);  // first halo column, 16-aligned
     const void* fs = sb::sweep_ptr_stream_f32(k);
     const size_t smem = (size_t)sb::NPROD * 2 * 8 * (sb::CW * sizeof(float) + sb::SRB_PAD) +
                         (size_t)sb::HB * sb::RLS * sizeof(int);
-    cudaError_t e = cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    FnFacts ff;
+    DevFacts df;
+    rc = launch_facts(fs, smem, &ff, &df);
+    if (rc) return rc;
     const int nb_total = (int)((all_rows + sb::HB - 1) / sb::HB);
-    const int gx = std::max(1, std::min(nb_total, sms * 2 * 8 / std::max(1, channels)));
+    const int gx = std::max(1, std::min(nb_total, df.sms * 2 * 8 / std::max(1, channels)));
     void* args[] = {(void*)&src, (void*)&mid, (void*)&g, (void*)&plan.taps, (void*)&xs, (void*)&nb_total,
                     (void*)&status_dev};
-    if (std::getenv("SB_DEBUG"))
-      std::fprintf(stderr, "[sliceblur_b200] stream rows: pmax=%d xs=%d lagc=%d bands=%d grid=%d x %d smem=%zu\n",
-                   plan.pmax, xs, lagc, nb_total, gx, channels, smem);
-    e = cudaLaunchKernel(fs, dim3(gx * channels, 1), dim3(sb::FUSED_THREADS), args, smem, st);
+    if (debug_plans())
+      std::fprintf(stderr, "[sliceblur_b200] stream rows: pmax=%d xs=%d bands=%d grid=%d x %d smem=%zu\n",
+                   plan.pmax, xs, nb_total, gx, channels, smem);
+    cudaError_t e = cudaLaunchKernel(fs, dim3(gx * channels, 1), dim3(sb::FUSED_THREADS), args, smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+  } else if (route.rows == RowPath::Tiled) {
+    const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);
+    Launch L1;
+    rc = plan_launch(f1, sb::Mode::RowsToMid, make_tiling(sb::Mode::RowsToMid, plan.pmax, channels, g.es, false),
+                     plan.pmax, g.W, all_rows, channels, &L1);
+    if (rc) return rc;
+    rc = launch_rows(f1, L1, src, mid, nullptr, g, plan.taps, status_dev, st);
+    if (rc) return rc;
   } else {
-  const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);
-  Launch L1;
-  rc = plan_launch(f1, sb::Mode::RowsToMid, make_tiling(sb::Mode::RowsToMid, plan.pmax, channels, g.es, false),
-                   plan.pmax, g.W, all_rows, channels, &L1);
-  if (rc) return rc;
-  rc = launch_rows(f1, L1, src, mid, nullptr, g, plan.taps, status_dev, st);
-  if (rc) return rc;
+    const size_t plane =
+        (size_t)batch * height * width * channels * (route.wide ? sizeof(long long) : sizeof(int));
+    void* scratch = route.scratch_bytes ? (void*)((char*)workspace + align256(plane)) : nullptr;
+    if (debug_plans())
+      std::fprintf(stderr, "[sliceblur_b200] generic rows: pmax=%d k=%d W=%d wide=%d scratch=%zu\n", plan.pmax, k,
+                   g.W, (int)route.wide, route.scratch_bytes);
+    const int e =
+        sb::launch_rows_generic(src, src_dtype, mid, nullptr, g, plan.tg, scratch, route.wide, status_dev, sms, st);
+    if (e) return cuda_fail((cudaError_t)e, "generic row pass");
   }
-  const void* f2 = pick_kernel(sb::Mode::ColsFromMid, src_dtype, k);
-  Launch L2;
-  sb::Tiling ct = make_tiling(sb::Mode::ColsFromMid, plan.pmax, channels, 4, false, (int)radii[0]);
-  // deep trails (older than the ring) of the largest boxes come through shared memory
-  ct.ndeep = 0;
-  for (int d = 0; d < sb::SB_NDEEP && d < k; ++d)
-    if (2 * sb::HB + plan.pmax + (int)radii[k - 1 - d] > ct.D) ct.ndeep = d + 1;
-  {
+
+  // ---- column pass
+  ColPath cols = route.cols;
+  if (cols == ColPath::Prefix) {
+    sb::Tiling ct = make_tiling(sb::Mode::ColsFromMid, plan.pmax, channels, 4, false), pt;
+    alignas(64) CUtensorMap mmap;
+    if (make_plane_map(mid, g, channels, &mmap) && cols_prefix_tiling(ct, radii, k, plan.pmax, &pt)) {
+      const void* f3 = sb::sweep_ptr_cols2(k);
+      Launch L3;
+      rc = plan_launch(f3, sb::Mode::ColsPrefix, pt, plan.pmax, g.W, total_rows, channels, &L3);
+      if (rc) return rc;
+      sb::Geometry g2 = g;
+      alignas(64) CUtensorMap omap;
+      make_output_map(dst, g2, &omap);
+      void* args[] = {(void*)&mid, (void*)&dst, (void*)&g2, (void*)&plan.taps, (void*)&L3.tl, (void*)&omap,
+                      (void*)&mmap};
+      // channels are folded into grid.x (fastest varying), as in cols_kernel
+      cudaError_t e = cudaLaunchKernel(f3, dim3(L3.grid.x * L3.grid.y), dim3(sb::C2THREADS), args, L3.smem, st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+      return SB_OK;
+    }
+    cols = running_cols_fits(radii, plan.pmax, channels) ? ColPath::Running : ColPath::Generic;
+  }
+  if (cols == ColPath::Running) {
+    const void* f2 = pick_kernel(sb::Mode::ColsFromMid, src_dtype, k);
+    sb::Tiling ct = make_tiling(sb::Mode::ColsFromMid, plan.pmax, channels, 4, false, (int)radii[0]);
+    // deep trails (older than the ring) of the largest boxes come through shared memory
+    ct.ndeep = 0;
+    for (int d = 0; d < sb::SB_NDEEP && d < k; ++d)
+      if (2 * sb::HB + plan.pmax + (int)radii[k - 1 - d] > ct.D) ct.ndeep = d + 1;
     const size_t band = (size_t)sb::HB * sb::WS * sizeof(int);
     const size_t budget = (512 / ct.tmem_cols) > 1 ? 100 * 1024 : 200 * 1024;
-    const int choices[] = {8, 6, 4, 3, 2};
     ct.pf = 2;
-    for (int pf : choices)
+    for (int pf : {8, 6, 4, 3, 2})
       if ((size_t)(1 + ct.ndeep) * pf * band <= budget) {
         ct.pf = pf;
         break;
       }
-  }
-  sb::Tiling pt;
-  alignas(64) CUtensorMap mmap;
-  if (make_plane_map(mid, g, channels, &mmap) && cols_prefix_tiling(ct, radii, k, plan.pmax, &pt)) {
-    const void* f3 = sb::sweep_ptr_cols2(k);
-    Launch L3;
-    rc = plan_launch(f3, sb::Mode::ColsPrefix, pt, plan.pmax, g.W, total_rows, channels, &L3);
+    Launch L2;
+    rc = plan_launch(f2, sb::Mode::ColsFromMid, ct, plan.pmax, g.W, total_rows, channels, &L2);
     if (rc) return rc;
-    sb::Geometry g2 = g;
-    alignas(64) CUtensorMap omap;
-    make_output_map(dst, g2, &omap);
-    void* args[] = {(void*)&mid, (void*)&dst, (void*)&g2, (void*)&plan.taps, (void*)&L3.tl, (void*)&omap, (void*)&mmap};
-    // channels are folded into grid.x (fastest varying), as in cols_kernel
-    cudaError_t e = cudaLaunchKernel(f3, dim3(L3.grid.x * L3.grid.y), dim3(sb::C2THREADS), args, L3.smem, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
-    return SB_OK;
+    return launch_cols(f2, L2, mid, dst, g, plan.taps, st);
   }
-  rc = plan_launch(f2, sb::Mode::ColsFromMid, ct, plan.pmax, g.W, total_rows, channels, &L2);
-  if (rc) return rc;
-  return launch_cols(f2, L2, mid, dst, g, plan.taps, st);
+  if (debug_plans()) std::fprintf(stderr, "[sliceblur_b200] generic cols: pmax=%d k=%d\n", plan.pmax, k);
+  const int e = sb::launch_cols_generic(mid, dst, g, plan.tg, route.wide, sms, st);
+  if (e) return cuda_fail((cudaError_t)e, "generic column pass");
+  return SB_OK;
 }
 
 int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_t height, int64_t width,
@@ -686,9 +836,16 @@ int sb_separable_filter_2d(const void* src, int src_dtype, int64_t batch, int64_
                                        weights, k, value_bound, workspace, workspace_bytes, status_dev, stream);
 }
 
+size_t sb_filter_rows_workspace_bytes(int src_dtype, int64_t rows, int64_t width, const int64_t* radii, int k) {
+  if (!radii || k < 1 || k > SB_MAX_K || rows < 1 || width < 1 || width > 0x7fffffff) return 0;
+  if (dtype_size(src_dtype) == 0 || radii[k - 1] < 0 || radii[k - 1] > 0x7fffffff) return 0;
+  if (route_rows_only(src_dtype, width, k, (int)radii[k - 1]) != RowPath::Generic) return 0;
+  return sb::generic_rows_scratch_bytes((int)width, needs_wide((int)radii[k - 1]));
+}
+
 int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, int64_t src_row_stride, float* dst,
                    int64_t dst_row_stride, const int64_t* radii, const double* weights, int k, double value_bound,
-                   int* status_dev, void* stream) {
+                   void* workspace, size_t workspace_bytes, int* status_dev, void* stream) {
   if (!src || !dst) return fail(SB_ERR_INVALID_ARGUMENT, "src/dst must not be NULL");
   if (rows < 1 || width < 1) return fail(SB_ERR_INVALID_ARGUMENT, "need a non-empty signal");
   if (rows > 0x7fffffff || width > 0x7fffffff) return fail(SB_ERR_INVALID_ARGUMENT, "extent exceeds int32");
@@ -696,8 +853,9 @@ int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, 
     return fail(SB_ERR_INVALID_ARGUMENT, "row stride smaller than width");
   int rc = sb_check_kernel(radii, weights, k, width);
   if (rc) return rc;
-  Plan plan;
-  rc = make_taps(radii, weights, k, src_dtype, value_bound, &plan);
+  const bool wide = needs_wide((int)radii[k - 1]);
+  static thread_local Plan plan;
+  rc = make_taps(radii, weights, k, src_dtype, value_bound, &plan, wide);
   if (rc) return rc;
   sb::Geometry g;
   std::memset(&g, 0, sizeof(g));
@@ -710,18 +868,29 @@ int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, 
   g.W = (int)width;
   g.nimg = 1;
   g.aligned16 = ((uintptr_t)src % 16 == 0) && ((src_row_stride * g.es) % 16 == 0);
-  const void* fn = pick_kernel(sb::Mode::RowsToOut, src_dtype, k);
-  Launch L;
-  rc = plan_launch(fn, sb::Mode::RowsToOut, make_tiling(sb::Mode::RowsToOut, plan.pmax, 1, g.es, false), plan.pmax,
-                   g.W, rows, 1, &L);
-  if (rc) return rc;
-  return launch_rows(fn, L, src, nullptr, dst, g, plan.taps, status_dev, (cudaStream_t)stream);
+  if (route_rows_only(src_dtype, width, k, plan.pmax) == RowPath::Tiled) {
+    const void* fn = pick_kernel(sb::Mode::RowsToOut, src_dtype, k);
+    Launch L;
+    rc = plan_launch(fn, sb::Mode::RowsToOut, make_tiling(sb::Mode::RowsToOut, plan.pmax, 1, g.es, false),
+                     plan.pmax, g.W, rows, 1, &L);
+    if (rc) return rc;
+    return launch_rows(fn, L, src, nullptr, dst, g, plan.taps, status_dev, (cudaStream_t)stream);
+  }
+  const size_t need = sb_filter_rows_workspace_bytes(src_dtype, rows, width, radii, k);
+  if (need && (!workspace || workspace_bytes < need))
+    return fail(SB_ERR_WORKSPACE, "workspace of " + std::to_string(need) + " bytes required");
+  const int e = sb::launch_rows_generic(src, src_dtype, nullptr, dst, g, plan.tg, need ? workspace : nullptr, wide,
+                                        status_dev, device_sms(), (cudaStream_t)stream);
+  if (e) return cuda_fail((cudaError_t)e, "generic row pass");
+  return SB_OK;
 }
 
 int sb_slice_filter_1d(const void* src, int src_dtype, int64_t n, float* dst, const int64_t* radii,
-                       const double* weights, int k, double value_bound, int* status_dev, void* stream) {
+                       const double* weights, int k, double value_bound, void* workspace, size_t workspace_bytes,
+                       int* status_dev, void* stream) {
   if (n < 1) return fail(SB_ERR_INVALID_ARGUMENT, "need a non-empty 1D signal");
-  return sb_filter_rows(src, src_dtype, 1, n, n, dst, n, radii, weights, k, value_bound, status_dev, stream);
+  return sb_filter_rows(src, src_dtype, 1, n, n, dst, n, radii, weights, k, value_bound, workspace, workspace_bytes,
+                        status_dev, stream);
 }
 
 }  // extern "C"

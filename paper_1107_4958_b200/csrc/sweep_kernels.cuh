@@ -66,14 +66,29 @@ struct Geometry {
   int out_bulk;                // one channel, 16-byte aligned rows: full output bands leave by TMA tensor stores
 };
 
+constexpr int FAST_K = 8;  // the templated sweep kernels take k <= FAST_K slices
+
 struct Taps {
   int k, pmax;
+  int p[FAST_K];
+  float w_row[FAST_K];   // w_i * 2^(s_mid - s_in): pass 1 output in mid quanta
+  float w_col[FAST_K];   // w_i * 2^-s_mid: pass 2 output in pixel units
+  float w_out1[FAST_K];  // w_i * 2^-s_in: pass 1 output in pixel units (row-only mode)
+  float in_scale;        // 2^s_in (float sources)
+  float in_limit;        // float sources: |x| * in_scale <= in_limit (the caller's bound, scaled; < 2^22)
+                         // uint16: x <= in_limit
+  float seen_limit;      // float sources: |x| * in_scale >= seen_limit (half the bound) sets SB_STATUS_HALF
+};
+
+// The same quanta for any k <= SB_MAX_K (generic two-pass kernels, filter_at): passed by
+// value (16 KB of kernel parameters, within the 32 KB sm_70+/CUDA 12.1 limit).
+struct TapsG {
+  int k, pmax;
+  float in_scale, in_limit, seen_limit;
   int p[SB_MAX_K];
-  float w_row[SB_MAX_K];   // w_i * 2^(s_mid - s_in): pass 1 output in mid quanta
-  float w_col[SB_MAX_K];   // w_i * 2^-s_mid: pass 2 output in pixel units
-  float w_out1[SB_MAX_K];  // w_i * 2^-s_in: pass 1 output in pixel units (row-only mode)
-  float in_scale;          // 2^s_in (float sources)
-  float in_limit;          // |x| * in_scale must be < in_limit (2^22)
+  float w_row[SB_MAX_K];
+  float w_col[SB_MAX_K];
+  float w_out1[SB_MAX_K];
 };
 
 struct Tiling {
@@ -265,19 +280,30 @@ struct SrcTraits<double> {
   static constexpr bool kFloat = true;
 };
 
-// fixed-point value of one source element; `bad` collects range violations
-template <typename T>
-__device__ __forceinline__ int to_fixed(T v, const Taps& t, bool& bad) {
+// fixed-point value of one source element; `st` collects status bits: SB_STATUS_RANGE
+// (above the caller's bound, or not finite) and SB_STATUS_HALF (at least half the bound)
+template <typename T, typename TT>
+__device__ __forceinline__ int to_fixed(T v, const TT& t, uint32_t& st) {
   if constexpr (SrcTraits<T>::kFloat) {
     float s = (float)v * t.in_scale;
-    bool ok = fabsf(s) < t.in_limit;  // false for NaN too
-    bad |= !ok;
+    const float a = fabsf(s);
+    const bool ok = a <= t.in_limit;  // false for NaN too
+    st |= ok ? 0u : (uint32_t)SB_STATUS_RANGE;
+    st |= a >= t.seen_limit ? (uint32_t)SB_STATUS_HALF : 0u;
     s = ok ? s : 0.0f;
     return __float_as_int(s + kMagic) - kMagicBits;  // round-to-nearest-even of v * 2^s_in
   } else {
-    if constexpr (sizeof(T) == 2) bad |= (float)v > t.in_limit;  // uint16 above the caller's bound
+    if constexpr (sizeof(T) == 2) st |= (float)v > t.in_limit ? (uint32_t)SB_STATUS_RANGE : 0u;
     return (int)v;
   }
+}
+
+// OR a thread's status bits into the caller's word: one atomic per bit the word lacks
+// (the HALF bit is seen by most threads of a typical image)
+__device__ __forceinline__ void report_status(int* status, uint32_t st) {
+  if (!st || !status) return;
+  const uint32_t have = (uint32_t)*(volatile int*)status;
+  if (st & ~have) atomicOr(status, (int)st);
 }
 
 // ---------------------------------------------------------------- pass 1: staging
@@ -353,7 +379,7 @@ __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restr
   const int rows_per_warp = 32 / lpr;
   const int sub = lane / lpr, sl = lane - sub * lpr;
   const int nchunk = tl.L / CH;
-  bool bad = false;
+  uint32_t bad = 0;
   for (int r0 = warp * rows_per_warp; r0 < n; r0 += nwarps * rows_per_warp) {
     const int r = r0 + sub;
     int running = 0;  // prefix of the chunk groups already done (rows longer than lpr chunks)
@@ -401,7 +427,7 @@ __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restr
       running += __shfl_sync(0xffffffffu, inc, lpr - 1, lpr);
     }
   }
-  if (bad && status) atomicOr(status, SB_STATUS_RANGE);
+  report_status(status, bad);
 }
 
 // The same scan for one warp over a whole band, bank-conflict free: lane (rr, cq)
@@ -416,7 +442,7 @@ __device__ __forceinline__ void scan_band8(const unsigned char* buf, int* __rest
   const int lane = threadIdx.x & 31;
   const int rr = lane & 7, cq = lane >> 3;
   const int nchunk = tl.L / CH;
-  bool bad = false;
+  uint32_t bad = 0;
   for (int r0 = 0; r0 < n; r0 += 8) {
     const int r = r0 + rr;
     int running = 0;
@@ -461,7 +487,7 @@ __device__ __forceinline__ void scan_band8(const unsigned char* buf, int* __rest
       running += __shfl_sync(0xffffffffu, inc, rr + 24);
     }
   }
-  if (bad && status) atomicOr(status, SB_STATUS_RANGE);
+  report_status(status, bad);
 }
 
 // uint8, one channel, float prefixes: rows q and q+8 of the band share float2 q of
@@ -1741,7 +1767,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
       // CH-column chunks; the row's running prefix (carry) lives in the 4 lanes of that row
       int carry = 0;
       issue(0, 0);
-      bool bad = false;
+      uint32_t bad = 0;
       for (int j = 0; j < nin; ++j) {
         const uint32_t gj = cin_ctr + j;
         cp_async_wait_all();
@@ -1778,7 +1804,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
         }
         mbar_arrive(&bar_full[gj % NSLOT]);
       }
-      if (bad && status) atomicOr(status, SB_STATUS_RANGE);
+      report_status(status, bad);
     } else {
       const int c = threadIdx.x;
       int* midrow[HB];  // destination rows of this band - hoisted
@@ -1861,8 +1887,17 @@ const void* sweep_ptr_u16(Mode m, int k);
 const void* sweep_ptr_f32(Mode m, int k);
 const void* sweep_ptr_f64(Mode m, int k);
 int launch_filter_at(const void* src, int src_dtype, long long row_stride, int H, int W, const int* cols, int ncols,
-                     const int* pt_col, const int* pt_y, long long npts, float* out, int* R, const Taps& t, int* status,
-                     cudaStream_t st);  // filter_at.cu
+                     const int* pt_col, const int* pt_y, long long npts, float* out, int* R, const TapsG& t,
+                     int* status, cudaStream_t st);  // filter_at.cu
+// generic two-pass kernels (generic_kernels.cu): any radius < extent, any k <= SB_MAX_K
+constexpr size_t kGenericSmemBytes = 200 * 1024;  // longest row prefix the row kernel keeps in shared memory
+constexpr int kGenericScratchRows = 296;          // global scratch rows (CTAs) for longer rows
+constexpr int kWideSpan = 2048;                   // 2*pmax+1 above this: int64 ("wide") generic arithmetic
+size_t generic_rows_scratch_bytes(int W, bool wide);
+int launch_rows_generic(const void* src, int src_dtype, void* mid_out, float* dst, const Geometry& g,
+                        const TapsG& t, void* scratch, bool wide, int* status, int sms, cudaStream_t st);
+int launch_cols_generic(void* mid, float* dst, const Geometry& g, const TapsG& t, bool wide, int sms,
+                        cudaStream_t st);
 const void* sweep_ptr_cols(int k);   // ColsFromMid (source type unused)
 const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)

@@ -14,8 +14,14 @@ Differences from the reference, by design:
   ``torch.Tensor`` objects (filtered in place on the device, result returned
   as a CUDA tensor);
 * float inputs are quantised to int32 fixed point with a quantum derived from
-  ``value_bound`` (max |pixel|).  When it is not given, it is measured on the
-  device.  A pixel above the bound raises ``ValueError``, never a wrong answer.
+  ``value_bound`` (max |pixel|).  A pixel above the bound raises ``ValueError``,
+  never a wrong answer.  When no bound is given, the previous image's measured
+  maximum (per source dtype) is used as a guess and validated by the kernels'
+  status word, which the call reads anyway (``SB_STATUS_RANGE`` clear and
+  ``SB_STATUS_HALF`` set: the quantum is within one bit of the measured one);
+  otherwise the maximum is measured on the device and the filter re-run.  So the
+  reference signature ``separable_filter_2d(img, kern)`` costs no extra pass over
+  the image in steady state.
 """
 
 from __future__ import annotations
@@ -110,7 +116,7 @@ def _check_kernel(kernel: SliceKernel, n: int):
     if abs(info[6] - 1.0) > _DC_TOL:
         raise ValueError("kernel must have unit DC gain; call normalized()")
     if kernel.k > nat.SB_MAX_K:
-        raise ValueError(f"at most {nat.SB_MAX_K} slices are supported on the GPU path")
+        raise ValueError(f"at most {nat.SB_MAX_K} slices are supported")
 
 
 class _Device:
@@ -151,17 +157,8 @@ class _Device:
         self.code = codes[self.tensor.dtype]
         self.stream = torch.cuda.current_stream().cuda_stream
 
-    def value_bound(self, given):
-        if self.code == nat.SB_DTYPE_U8:
-            return 0.0  # exact integer path; bound implied by the dtype
-        if self.code == nat.SB_DTYPE_U16 and given is None:
-            # exact samples either way; the measured maximum only refines the row-value quantum
-            out = self.torch.zeros(1, dtype=self.torch.float64, device=self.tensor.device)
-            _raise_for(nat.load().sb_max_abs(self.tensor.data_ptr(), self.code, self.tensor.numel(), out.data_ptr(),
-                                              self.stream))
-            return max(1.0, float(out.item()))
-        if given is not None:
-            return float(given)
+    def measure_max(self) -> float:
+        """max |pixel| on the device (one read of the input and a host sync)."""
         out = self.torch.zeros(1, dtype=self.torch.float64, device=self.tensor.device)
         _raise_for(nat.load().sb_max_abs(self.tensor.data_ptr(), self.code, self.tensor.numel(), out.data_ptr(),
                                           self.stream))
@@ -170,9 +167,44 @@ class _Device:
             raise ValueError("input contains NaN or Inf; the fixed-point GPU path needs finite pixels")
         return bound
 
-    def finish(self, result, status, check: bool, host_out=None):
-        if check and int(status.item()) & nat.SB_STATUS_RANGE:
+    def bound_for(self, given, check: bool):
+        """(value_bound for the ABI, speculative?) - see the module docstring."""
+        if self.code == nat.SB_DTYPE_U8:
+            return 0.0, False  # exact integer path; bound implied by the dtype
+        if given is not None:
+            return float(given), False
+        if self.code == nat.SB_DTYPE_U16:
+            # exact samples either way; the measured maximum only refines the row-value quantum
+            return max(1.0, self.measure_max()), False
+        if check and self.code in _BOUND_GUESS:
+            return _BOUND_GUESS[self.code], True
+        bound = self.measure_max()
+        _BOUND_GUESS[self.code] = bound
+        return bound, False
+
+    def run(self, launch, value_bound, check: bool, status=None):
+        """launch(bound, status_ptr) -> ABI code; validates the status word once."""
+        torch = self.torch
+        own = status is None and check
+        if own:
+            status = torch.zeros(1, dtype=torch.int32, device=self.tensor.device)
+        bound, spec = self.bound_for(value_bound, check)
+        sp = status.data_ptr() if status is not None else None
+        _raise_for(launch(bound, sp))
+        if not own:
+            return
+        st = int(status.item())
+        if spec and (st & nat.SB_STATUS_RANGE or not st & nat.SB_STATUS_HALF):
+            # the guess does not fit this image: measure it and filter again
+            bound = self.measure_max()
+            _BOUND_GUESS[self.code] = bound
+            status.zero_()
+            _raise_for(launch(bound, sp))
+            st = int(status.item())
+        if st & nat.SB_STATUS_RANGE:
             raise ValueError("a pixel exceeds value_bound (or is not finite)")
+
+    def finish(self, result, host_out=None):
         if host_out is not None:
             host_out.copy_(result.view(host_out.shape))
             return host_out
@@ -183,16 +215,26 @@ class _Device:
         return result
 
 
+# last measured max |pixel| per float source dtype (the speculative bound, see above)
+_BOUND_GUESS: "dict[int, float]" = {}
+
+
+def _overlaps(a, b) -> bool:
+    a0, b0 = a.data_ptr(), b.data_ptr()
+    return a0 < b0 + b.numel() * b.element_size() and b0 < a0 + a.numel() * a.element_size()
+
+
 def separable_filter_batch(images, kernel: SliceKernel, *, channels_last: bool = False, value_bound=None,
-                           out=None, check: bool = True):
+                           out=None, check: bool = True, _status=None):
     """Filter a batch of images: (B, H, W) or, with ``channels_last``,
     (B, H, W, C) / (H, W, C) with interleaved channels each filtered separately.
 
     The per-image arithmetic is ``separable_filter_2d``'s (filtering.py:76-104).
     Returns float32 of the input's shape (numpy in -> numpy out, CUDA tensor in
     -> CUDA tensor out, host tensor in -> host tensor out).  ``out`` may supply a
-    preallocated contiguous float32 tensor: on the GPU it is written in place,
-    on the host (ideally pinned) the result is copied into it.
+    preallocated contiguous float32 tensor of the input's shape: on the GPU it is
+    written in place (it must not overlap the input), on the host (ideally pinned)
+    the result is copied into it.
     """
     torch_mod = _torch()
     if (isinstance(images, torch_mod.Tensor) and not images.is_cuda and out is not None and not out.is_cuda
@@ -220,9 +262,11 @@ def separable_filter_batch(images, kernel: SliceKernel, *, channels_last: bool =
     torch = dev.torch
     host_out = None
     if out is not None:
-        if out.dtype != torch.float32 or not out.is_contiguous() or out.numel() != x.numel():
-            raise ValueError("out must be a contiguous float32 tensor of the input's size")
+        if out.dtype != torch.float32 or not out.is_contiguous() or tuple(out.shape) != tuple(dev.tensor.shape):
+            raise ValueError("out must be a contiguous float32 tensor of the input's shape")
         if out.is_cuda:
+            if _overlaps(out, dev.tensor):
+                raise ValueError("out must not overlap the input (the sweeps read rows other CTAs write)")
             result = out
         else:
             host_out = out  # D2H into the caller's (pinned) host buffer
@@ -233,18 +277,16 @@ def separable_filter_batch(images, kernel: SliceKernel, *, channels_last: bool =
     lib = nat.load()
     ws_bytes = int(lib.sb_separable_filter_2d_workspace_bytes(dev.code, b, h, w, c, rp, kernel.k))
     workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device) if ws_bytes else None
-    # the range status word is only read when checking (the kernels skip it when NULL)
-    status = torch.zeros(1, dtype=torch.int32, device=x.device) if check else None
-    bound = dev.value_bound(value_bound)
-    code = lib.sb_separable_filter_2d(
-        x.data_ptr(), dev.code, b, h, w, c, h * w * c, w * c,
-        result.data_ptr(), h * w * c, w * c,
-        rp, wp, kernel.k, bound,
-        workspace.data_ptr() if workspace is not None else None, ws_bytes,
-        status.data_ptr() if status is not None else None, dev.stream,
-    )
-    _raise_for(code)
-    return dev.finish(result, status, check, host_out)
+
+    def launch(bound, status_ptr):
+        return lib.sb_separable_filter_2d(
+            x.data_ptr(), dev.code, b, h, w, c, h * w * c, w * c,
+            result.data_ptr(), h * w * c, w * c,
+            rp, wp, kernel.k, bound,
+            workspace.data_ptr() if workspace is not None else None, ws_bytes, status_ptr, dev.stream)
+
+    dev.run(launch, value_bound, check and _status is None, status=_status)
+    return dev.finish(result, host_out)
 
 
 def _pipelined_host_batch(images, kernel, channels_last, value_bound, out, check, chunks: int = 8):
@@ -252,15 +294,50 @@ def _pipelined_host_batch(images, kernel, channels_last, value_bound, out, check
 
     The batch is cut into ``chunks`` image groups; group i is copied in on one
     stream while group i-1 is filtered on another and group i-2 copied out on a
-    third (three device buffers rotate).  Every group is an independent
-    ``separable_filter_batch`` call, so the result is identical to the
-    one-shot call (float input without ``value_bound`` gets its bound per group).
+    third (three device buffers rotate).  Every group runs with the same quanta as
+    the one-shot call (float input: one bound for the whole batch - the caller's,
+    the speculative guess, or the measured maximum), so the result is identical to
+    it; the groups OR their status bits into one device word, read once at the end
+    (no host sync between groups).
     """
     torch = _torch()
     if not torch.cuda.is_available():
         raise RuntimeError("sliceblur_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
-    if out.dtype != torch.float32 or not out.is_contiguous() or out.numel() != images.numel():
-        raise ValueError("out must be a contiguous float32 tensor of the input's size")
+    if out.dtype != torch.float32 or not out.is_contiguous() or tuple(out.shape) != tuple(images.shape):
+        raise ValueError("out must be a contiguous float32 tensor of the input's shape")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    code = {torch.float32: nat.SB_DTYPE_F32, torch.float64: nat.SB_DTYPE_F64}.get(images.dtype)
+    is_float = code is not None
+    spec = False
+    bound = value_bound
+    if is_float and bound is None:
+        if check and code in _BOUND_GUESS:
+            bound, spec = _BOUND_GUESS[code], True
+        else:
+            bound = float(images.abs().max())
+            if not np.isfinite(bound):
+                raise ValueError("input contains NaN or Inf; the fixed-point GPU path needs finite pixels")
+            _BOUND_GUESS[code] = bound
+    status = torch.zeros(1, dtype=torch.int32, device=dev) if check else None
+    _run_pipeline(images, kernel, channels_last, bound, out, status, chunks)
+    if not check:
+        return out
+    st = int(status.item())
+    if spec and (st & nat.SB_STATUS_RANGE or not st & nat.SB_STATUS_HALF):
+        bound = float(images.abs().max())
+        if not np.isfinite(bound):
+            raise ValueError("input contains NaN or Inf; the fixed-point GPU path needs finite pixels")
+        _BOUND_GUESS[code] = bound
+        status.zero_()
+        _run_pipeline(images, kernel, channels_last, bound, out, status, chunks)
+        st = int(status.item())
+    if st & nat.SB_STATUS_RANGE:
+        raise ValueError("a pixel exceeds value_bound (or is not finite)")
+    return out
+
+
+def _run_pipeline(images, kernel, channels_last, bound, out, status, chunks):
+    torch = _torch()
     b = images.shape[0]
     chunks = max(1, min(chunks, b))
     bounds = [b * i // chunks for i in range(chunks + 1)]
@@ -289,8 +366,8 @@ def _pipelined_host_batch(images, kernel, channels_last, value_bound, out, check
             s_run.wait_event(ev_in)
             if done_out[k] is not None:
                 s_run.wait_event(done_out[k])  # output buffer k copied out
-            separable_filter_batch(xin[k][:n], kernel, channels_last=channels_last, value_bound=value_bound,
-                                   out=yout[k][:n], check=check)
+            separable_filter_batch(xin[k][:n], kernel, channels_last=channels_last, value_bound=bound,
+                                   out=yout[k][:n], check=status is not None, _status=status)
             done_run[k] = torch.cuda.Event()
             done_run[k].record(s_run)
         with torch.cuda.stream(s_out):
@@ -301,7 +378,6 @@ def _pipelined_host_batch(images, kernel, channels_last, value_bound, out, check
     for st in (s_in, s_run, s_out):
         main.wait_stream(st)
     s_out.synchronize()
-    return out
 
 
 def separable_filter_window(image, kernel: SliceKernel, row_begin: int, row_end: int, *, channels_last: bool = False,
@@ -335,17 +411,21 @@ def separable_filter_window(image, kernel: SliceKernel, row_begin: int, row_end:
     result = out if out is not None else torch.empty(shape, dtype=torch.float32, device=x.device)
     if result.dtype != torch.float32 or not result.is_cuda or not result.is_contiguous() or tuple(result.shape) != shape:
         raise ValueError("out must be a contiguous float32 CUDA tensor of shape %r" % (shape,))
+    if out is not None and _overlaps(result, x):
+        raise ValueError("out must not overlap the input")
     radii, weights, rp, wp = _kernel_arrays(kernel)
     lib = nat.load()
-    ws_bytes = lib.sb_separable_filter_2d_workspace_bytes(dev.code, 1, h, w, c, rp, kernel.k)
-    workspace = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=x.device)
-    status = torch.zeros(1, dtype=torch.int32, device=x.device)
-    bound = dev.value_bound(value_bound)
-    _raise_for(lib.sb_separable_filter_2d_window(
-        x.data_ptr(), dev.code, 1, h, w, c, h * w * c, w * c, row_begin, row_end,
-        result.data_ptr(), (row_end - row_begin) * w * c, w * c,
-        rp, wp, kernel.k, bound, workspace.data_ptr(), int(ws_bytes), status.data_ptr(), dev.stream))
-    return dev.finish(result, status, check)
+    ws_bytes = int(lib.sb_separable_filter_2d_workspace_bytes(dev.code, 1, h, w, c, rp, kernel.k))
+    workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
+
+    def launch(bound, status_ptr):
+        return lib.sb_separable_filter_2d_window(
+            x.data_ptr(), dev.code, 1, h, w, c, h * w * c, w * c, row_begin, row_end,
+            result.data_ptr(), (row_end - row_begin) * w * c, w * c,
+            rp, wp, kernel.k, bound, workspace.data_ptr(), ws_bytes, status_ptr, dev.stream)
+
+    dev.run(launch, value_bound, check)
+    return dev.finish(result)
 
 
 def separable_filter_2d(image, kernel: SliceKernel, parallel: bool = False, *, value_bound=None, out=None,
@@ -373,14 +453,24 @@ def filter_rows(arr, kernel: SliceKernel, *, value_bound=None, check: bool = Tru
         raise ValueError("need a non-empty 2D array")
     m, n = x.shape
     _check_kernel(kernel, n)
+    return _rows_only(dev, x, m, n, kernel, value_bound, check, (m, n))
+
+
+def _rows_only(dev, x, m, n, kernel, value_bound, check, shape):
     torch = dev.torch
-    result = torch.empty((m, n), dtype=torch.float32, device=x.device)
+    result = torch.empty(shape, dtype=torch.float32, device=x.device)
     radii, weights, rp, wp = _kernel_arrays(kernel)
-    status = torch.zeros(1, dtype=torch.int32, device=x.device)
-    bound = dev.value_bound(value_bound)
-    _raise_for(nat.load().sb_filter_rows(x.data_ptr(), dev.code, m, n, n, result.data_ptr(), n, rp, wp, kernel.k,
-                                         bound, status.data_ptr(), dev.stream))
-    return dev.finish(result, status, check)
+    lib = nat.load()
+    ws_bytes = int(lib.sb_filter_rows_workspace_bytes(dev.code, m, n, rp, kernel.k))
+    workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=x.device) if ws_bytes else None
+
+    def launch(bound, status_ptr):
+        return lib.sb_filter_rows(x.data_ptr(), dev.code, m, n, n, result.data_ptr(), n, rp, wp, kernel.k, bound,
+                                  workspace.data_ptr() if workspace is not None else None, ws_bytes, status_ptr,
+                                  dev.stream)
+
+    dev.run(launch, value_bound, check)
+    return dev.finish(result)
 
 
 def slice_filter_1d(signal, kernel: SliceKernel, *, value_bound=None, check: bool = True):
@@ -391,14 +481,7 @@ def slice_filter_1d(signal, kernel: SliceKernel, *, value_bound=None, check: boo
         raise ValueError("need a non-empty 1D signal")
     n = x.numel()
     _check_kernel(kernel, n)
-    torch = dev.torch
-    result = torch.empty(n, dtype=torch.float32, device=x.device)
-    radii, weights, rp, wp = _kernel_arrays(kernel)
-    status = torch.zeros(1, dtype=torch.int32, device=x.device)
-    bound = dev.value_bound(value_bound)
-    _raise_for(nat.load().sb_slice_filter_1d(x.data_ptr(), dev.code, n, result.data_ptr(), rp, wp, kernel.k, bound,
-                                             status.data_ptr(), dev.stream))
-    return dev.finish(result, status, check)
+    return _rows_only(dev, x, 1, n, kernel, value_bound, check, (n,))
 
 
 def prefix_sum(values):
@@ -466,9 +549,11 @@ def filter_at(image, kernel: SliceKernel, points, *, value_bound=None, check: bo
     lib = nat.load()
     ws_bytes = int(lib.sb_filter_at_workspace_bytes(h, len(cols)))
     workspace = torch.empty(max(ws_bytes, 4), dtype=torch.uint8, device=x.device)
-    status = torch.zeros(1, dtype=torch.int32, device=x.device)
-    bound = dev.value_bound(value_bound)
-    _raise_for(lib.sb_filter_at(x.data_ptr(), dev.code, h, w, w, cols_d.data_ptr(), len(cols), pt_col.data_ptr(),
+
+    def launch(bound, status_ptr):
+        return lib.sb_filter_at(x.data_ptr(), dev.code, h, w, w, cols_d.data_ptr(), len(cols), pt_col.data_ptr(),
                                 pt_y.data_ptr(), len(pts), result.data_ptr(), rp, wp, kernel.k, bound,
-                                workspace.data_ptr(), ws_bytes, status.data_ptr(), dev.stream))
-    return dev.finish(result, status, check)
+                                workspace.data_ptr(), ws_bytes, status_ptr, dev.stream)
+
+    dev.run(launch, value_bound, check)
+    return dev.finish(result)
