@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(128) filter_at_rows_kernel(const Tin* __restri
   if (y >= H) return;
   const int x = cols[ci];
   const Tin* row = src + (long long)y * row_stride;
-  uint32_t bad = 0;
+  RangeAcc bad;
   long long box = 0;  // int64: exact for the int32 quanta and for the wide (int64) ones alike
   int covered = -1;
   float acc = 0.0f;
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(128) filter_at_rows_kernel(const Tin* __restri
     acc = fmaf(t.w_row[i], __ll2float_rn(box), acc);
   }
   R[(long long)ci * H + y] = __float_as_int(acc + kMagic) - kMagicBits;
-  report_status(status, bad);
+  report_status(status, bad, t);
 }
 
 // out[n]: the column pass of column pt_col[n] at row pt_y[n] (exact wrapping int32

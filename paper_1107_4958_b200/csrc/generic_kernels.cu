@@ -39,6 +39,7 @@ constexpr int GITEMS = 8;  // elements per thread and scan step
 // elements f0 / fl.  Unsigned arithmetic: the boundary products may wrap.
 template <typename U, typename IdxFn>
 __device__ __forceinline__ U box_sum(IdxFn I, int x, int p, int n, U f0, U fl) {
+  SB_ASSERT(x >= 0 && x < n && p >= 0 && p < n);
   const long long xh = (long long)x + p;
   const U hi = xh < n ? (U)I((int)xh) : (U)I(n - 1) + (U)(xh - n + 1) * fl;
   const long long xl = (long long)x - p - 1;
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(GT) rows_generic_kernel(const Tin* __restrict_
   A* S = use_smem ? (A*)smem_raw : scratch + (long long)blockIdx.x * g.W;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long nrows = (long long)g.nimg * g.H * g.in_px;  // (image, row, channel)
-  uint32_t bad = 0;
+  RangeAcc bad;
   for (long long r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int ch = (int)(r % g.in_px);
     const long long ir = r / g.in_px;
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(GT) rows_generic_kernel(const Tin* __restrict_
     }
     __syncthreads();  // S is rewritten by the next row
   }
-  report_status(status, bad);
+  report_status(status, bad, t);
 }
 
 // Running column prefix of the int32 plane [channel][image][H][W], in place (wrapping).

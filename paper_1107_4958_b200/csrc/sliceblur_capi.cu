@@ -196,6 +196,8 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
   tl.stage_row_bytes = ceil16(tl.L * staged_ch * es);
   if (m == sb::Mode::Fused && (tl.stage_row_bytes / 16) % 2 == 0) tl.stage_row_bytes += 16;  // odd x 16 B: no conflicts
   tl.ls = (m == sb::Mode::Fused) ? sb::LS : tl.L;
+  if (m == sb::Mode::Fused && es == 4 && channels == 1 && !u8_single)  // float32: stride sized from L
+    tl.ls = tl.L <= sb::LS_SMALL ? sb::LS_SMALL : (tl.L <= sb::LS_MID ? sb::LS_MID : sb::LS);
   tl.packed = (m == sb::Mode::Fused && u8_single && ((tl.L + 63) & ~63) <= 192) ? 1 : 0;  // float2 prefixes
   if (tl.packed) {
     // the scan covers whole 64-column quarters; rows an odd multiple of 16 bytes apart
@@ -203,9 +205,10 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
     tl.stage_row_bytes = tl.L + 16;
   }
   tl.npb = 1;  // one prefix buffer per producer warp (each owns every FPROD-th band)
+  tl.nsb = (m == sb::Mode::Fused && es == 4 && tl.ls == sb::LS_SMALL) ? 1 : 2;  // mirrors fused_kernel's NSB
   if (m == sb::Mode::Fused) {
-    const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP2 * sizeof(float2) : (size_t)sb::HB * sb::LS * sizeof(int);
-    const size_t end = (size_t)2 * sb::FPROD * sb::HB * tl.stage_row_bytes + (size_t)sb::FPROD * tl.npb * pbuf;
+    const size_t pbuf = tl.packed ? (size_t)(sb::HB / 2) * sb::LSP2 * sizeof(float2) : (size_t)sb::HB * tl.ls * sizeof(int);
+    const size_t end = (size_t)tl.nsb * sb::FPROD * sb::HB * tl.stage_row_bytes + (size_t)sb::FPROD * tl.npb * pbuf;
     tl.obuf_off = (int)((end + 127) & ~(size_t)127);
   }
   tl.D = ((2 * pmax + 2 * sb::HB + sb::HB - 1) / sb::HB) * sb::HB;  // multiple of HB
@@ -255,7 +258,7 @@ size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
     // + FCONS x 2 output bands of HB x 32 floats staged for TMA tensor stores
     // output staging per consumer warp: 1 (three-CTA), 2 (two-CTA) 16-row boxes, or two 32-row boxes (split 5)
-    const int boxes = tl.split == 3 ? 1 : (tl.split == 5 ? 4 : 2);
+    const int boxes = tl.split == 3 ? 1 : (tl.split == 5 ? 4 : tl.nsb);
     size_t s = (size_t)tl.obuf_off + 128 + (size_t)sb::FCONS * boxes * sb::HB * 32 * sizeof(float);
     // cap residency at 512 / tmem_cols CTAs per SM by asking for enough shared
     // memory, so no CTA ever waits inside tcgen05.alloc
@@ -317,13 +320,14 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
     if (!ok) continue;
     tl.ds = thr >= 0 ? 2 * tl.lag - NB - span + 2 : 0;  // >= lag - NB + copy_e, plus one spare
     tl.pf = 0;
-    for (int pf : {sb::C2PF, 6, 4, 3, 2})  // slots of two bands each
-      if ((size_t)(2 * pf + tl.ds) * band + obuf <= kSmemBudget) {
+    const int copies = tl.ds ? tl.ds + 1 : 0;  // + the mirror of copy slot 0
+    for (int pf : {sb::C2PF, 6, 4, 3, 2})      // slots of two bands each
+      if ((size_t)(2 * pf + copies) * band + obuf <= kSmemBudget) {
         tl.pf = pf;
         break;
       }
     if (!tl.pf) continue;
-    tl.obuf_off = (int)((size_t)(2 * tl.pf + tl.ds) * band);
+    tl.obuf_off = (int)((size_t)(2 * tl.pf + copies) * band);
     *out = tl;
     return true;
   }
@@ -721,7 +725,8 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     const sb::Tiling base = make_tiling(sb::Mode::Fused, plan.pmax, channels, g.es, u8_single);
     const void* fn = base.split == 3   ? sb::sweep_ptr_fused3(k)
                      : base.split == 5 ? sb::sweep_ptr_fused5(k)
-                                       : pick_kernel(sb::Mode::Fused, src_dtype, k);
+                     : (src_dtype == SB_DTYPE_F32 && channels == 1) ? sb::sweep_ptr_fused_f32(k, base.ls)
+                                                                     : pick_kernel(sb::Mode::Fused, src_dtype, k);
     Launch L;
     rc = plan_launch(fn, sb::Mode::Fused, base, plan.pmax, g.W, total_rows, channels, &L);
     if (rc) return rc;

@@ -35,6 +35,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -47,6 +48,10 @@ constexpr int WS = 128;         // strip width = threads per CTA
 constexpr int NWARPS = WS / 32;
 constexpr int CH = 16;          // px per scan chunk (one lane)
 constexpr int LS = 516;         // fused prefix row stride in words (compile-time offsets; 2064 B = 16 mod 128)
+// float32 sources pick the smallest of these strides >= L (all 16 mod 128 bytes, so the
+// 8-row phases of the prefix stores stay conflict-free): small radii then fit two CTAs' or
+// one CTA's shared memory with the f32 staging (C1, C2)
+constexpr int LS_SMALL = 196, LS_MID = 324;
 constexpr int LMAX = 512;       // longest staged / prefix row of the fused sweep
 constexpr int LSP2 = 194;       // uint8 float2-prefix row stride (L <= 192): 1552 B = 16 (mod 128), conflict-free
 constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: x + kMagic rounds x to an integer (|x| < 2^22)
@@ -112,9 +117,42 @@ struct Tiling {
   int lag;              // cols2: ring band v is written once output band v - lag is done
   int copy_e;           // cols2: band v - D/HB + copy_e is copied out of the ring while band v is written
   int split;            // fused: 3 = three-CTA-per-SM variant (fused_kernel<uint8_t, K, 3>)
+  int nsb;              // fused: staged bands per producer warp (1 or 2; the output box is buffered alike)
 };
 
 enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3, ColsPrefix = 4 };
+
+// ---------------------------------------------------------------- checked build
+// SB_CHECKED (tools/build_checked.py): device-side bounds traps at the shared-memory / TMEM
+// indexing points, and a pseudo-random sleep (0-1 us, from %globaltimer) at every hand-off
+// (mbarrier arrive / wait, named barrier, bulk-store wait) so each run interleaves the
+// producer, consumer and TMA traffic differently; tools/checked_run.py then requires
+// bit-identical results across runs and agreement with the oracle.  compute-sanitizer is
+// closed on this pool, so this is the race / bounds check.
+#ifdef SB_CHECKED
+__device__ __forceinline__ void sb_perturb() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  uint32_t h = (uint32_t)t * 2654435761u ^ (threadIdx.x * 40503u) ^ (blockIdx.x * 2246822519u);
+  h ^= h >> 15;
+  h *= 2246822519u;
+  h ^= h >> 13;
+  if ((h & 3) == 0) __nanosleep((h >> 8) & 1023);
+}
+#define SB_ASSERT(c)                                                                                      \
+  do {                                                                                                    \
+    if (!(c)) {                                                                                           \
+      printf("SB_ASSERT %s failed at %s:%d block %d thread %d\n", #c, __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                           \
+      __trap();                                                                                           \
+    }                                                                                                     \
+  } while (0)
+#else
+__device__ __forceinline__ void sb_perturb() {}
+#define SB_ASSERT(c) \
+  do {               \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- small helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -162,6 +200,7 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+  sb_perturb();
 }
 
 // ---- tensor memory (tcgen05): the fused column ring.  Thread c of the CTA owns
@@ -221,6 +260,7 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  sb_perturb();
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
                : "memory");
 }
@@ -230,6 +270,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+  sb_perturb();
 }
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -248,8 +289,10 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
     __nanosleep(ns);
     ns = ns < 1024 ? 2 * ns : ns;
   }
+  sb_perturb();
 }
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  sb_perturb();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
@@ -280,28 +323,46 @@ struct SrcTraits<double> {
   static constexpr bool kFloat = true;
 };
 
-// fixed-point value of one source element; `st` collects status bits: SB_STATUS_RANGE
-// (above the caller's bound, or not finite) and SB_STATUS_HALF (at least half the bound)
+// Range of the source elements a thread converted: the NaN-propagating max |x| of float
+// sources (one FMNMX per element), turned into status bits once per thread by
+// report_status; uint16 sources set SB_STATUS_RANGE directly.
+struct RangeAcc {
+  float m = 0.0f;
+  uint32_t st = 0;
+};
+
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+
+// fixed-point value of one source element: round(x * 2^s_in) by the magic-number FFMA
+// (x * 2^s_in is exact, so this is the rounding of the exact product); an element past the
+// caller's bound (or NaN / Inf) gives an unspecified value and is reported, never hidden
 template <typename T, typename TT>
-__device__ __forceinline__ int to_fixed(T v, const TT& t, uint32_t& st) {
+__device__ __forceinline__ int to_fixed(T v, const TT& t, RangeAcc& r) {
   if constexpr (SrcTraits<T>::kFloat) {
-    float s = (float)v * t.in_scale;
-    const float a = fabsf(s);
-    const bool ok = a <= t.in_limit;  // false for NaN too
-    st |= ok ? 0u : (uint32_t)SB_STATUS_RANGE;
-    st |= a >= t.seen_limit ? (uint32_t)SB_STATUS_HALF : 0u;
-    s = ok ? s : 0.0f;
-    return __float_as_int(s + kMagic) - kMagicBits;  // round-to-nearest-even of v * 2^s_in
+    const float f = (float)v;
+    r.m = fmax_nan(r.m, fabsf(f));
+    return __float_as_int(fmaf(f, t.in_scale, kMagic)) - kMagicBits;
   } else {
-    if constexpr (sizeof(T) == 2) st |= (float)v > t.in_limit ? (uint32_t)SB_STATUS_RANGE : 0u;
+    if constexpr (sizeof(T) == 2) r.st |= (float)v > t.in_limit ? (uint32_t)SB_STATUS_RANGE : 0u;
     return (int)v;
   }
 }
 
-// OR a thread's status bits into the caller's word: one atomic per bit the word lacks
-// (the HALF bit is seen by most threads of a typical image)
-__device__ __forceinline__ void report_status(int* status, uint32_t st) {
-  if (!st || !status) return;
+// OR a thread's status bits into the caller's word: SB_STATUS_RANGE (an element above the
+// caller's bound, or not finite), SB_STATUS_HALF (one at least half the bound); one atomic
+// per bit the word lacks (the HALF bit is seen by most threads of a typical image)
+template <typename TT>
+__device__ __forceinline__ void report_status(int* status, const RangeAcc& r, const TT& t) {
+  if (!status) return;
+  const float s = r.m * t.in_scale;  // exact (power of two); NaN stays NaN
+  uint32_t st = r.st;
+  st |= s <= t.in_limit ? 0u : (uint32_t)SB_STATUS_RANGE;
+  st |= s >= t.seen_limit ? (uint32_t)SB_STATUS_HALF : 0u;
+  if (!st) return;
   const uint32_t have = (uint32_t)*(volatile int*)status;
   if (st & ~have) atomicOr(status, (int)st);
 }
@@ -323,6 +384,7 @@ __device__ __forceinline__ void issue_stage(unsigned char* buf, const Tin* __res
       const int r = fast_div(idx, chunk_magic), q = idx - r * nchunk;
       const int v = min(max(v0 + r, 0), g.H - 1);
       const unsigned char* grow = (const unsigned char*)(src_img + (long long)v * g.in_row);
+      SB_ASSERT(lo + 16 * q - base >= 0 && lo + 16 * q - base + 16 <= tl.stage_row_bytes && r < HB);
       cp_async16(buf + r * tl.stage_row_bytes + (lo + 16 * q - base), grow + lo + 16 * q);
     }
     cp_async_commit();
@@ -379,7 +441,7 @@ __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restr
   const int rows_per_warp = 32 / lpr;
   const int sub = lane / lpr, sl = lane - sub * lpr;
   const int nchunk = tl.L / CH;
-  uint32_t bad = 0;
+  RangeAcc bad;
   for (int r0 = warp * rows_per_warp; r0 < n; r0 += nwarps * rows_per_warp) {
     const int r = r0 + sub;
     int running = 0;  // prefix of the chunk groups already done (rows longer than lpr chunks)
@@ -427,7 +489,7 @@ __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restr
       running += __shfl_sync(0xffffffffu, inc, lpr - 1, lpr);
     }
   }
-  report_status(status, bad);
+  report_status(status, bad, t);
 }
 
 // The same scan for one warp over a whole band, bank-conflict free: lane (rr, cq)
@@ -436,13 +498,13 @@ __device__ __forceinline__ void scan_rows(const unsigned char* buf, int* __restr
 // chunk, which sit in 8 distinct bank groups (row strides are an odd multiple of
 // 16 bytes); the row prefix of the chunk groups already done is carried in the
 // row's 4 lanes.
-template <typename Tin>
+template <typename Tin, int PLS = LS>
 __device__ __forceinline__ void scan_band8(const unsigned char* buf, int* __restrict__ P, const Geometry& g,
                                            const Taps& t, const Tiling& tl, int ch, int n, int* status) {
   const int lane = threadIdx.x & 31;
   const int rr = lane & 7, cq = lane >> 3;
   const int nchunk = tl.L / CH;
-  uint32_t bad = 0;
+  RangeAcc bad;
   for (int r0 = 0; r0 < n; r0 += 8) {
     const int r = r0 + rr;
     int running = 0;
@@ -479,7 +541,7 @@ __device__ __forceinline__ void scan_band8(const unsigned char* buf, int* __rest
       if (cq >= 2) inc += y;
       const int carry = running + inc - tot;
       if (live) {
-        int4* dst = (int4*)(P + r * LS + chunk * CH);
+        int4* dst = (int4*)(P + r * PLS + chunk * CH);
 #pragma unroll
         for (int m = 0; m < CH / 4; ++m)
           dst[m] = make_int4(v[4 * m] + carry, v[4 * m + 1] + carry, v[4 * m + 2] + carry, v[4 * m + 3] + carry);
@@ -487,7 +549,7 @@ __device__ __forceinline__ void scan_band8(const unsigned char* buf, int* __rest
       running += __shfl_sync(0xffffffffu, inc, rr + 24);
     }
   }
-  report_status(status, bad);
+  report_status(status, bad, t);
 }
 
 // uint8, one channel, float prefixes: rows q and q+8 of the band share float2 q of
@@ -563,6 +625,7 @@ __device__ __forceinline__ void band_rows(const int* __restrict__ P, int c, cons
 #pragma unroll
   for (int r = 0; r < HB; ++r) acc[r] = 0.0f;
   const int base = c + tl.xoff;
+  SB_ASSERT(base - t.p[K - 1] - 1 >= 0 && base + t.p[K - 1] < tl.L && tl.L <= ls);
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     const int* pl = P + base + t.p[i];
@@ -579,6 +642,7 @@ template <int K>
 __device__ __forceinline__ void band_rows_f2(const float2* __restrict__ P, int c, const Taps& t, const Tiling& tl,
                                              float2 (&acc)[HB / 2]) {
   const int base = c + tl.xoff;
+  SB_ASSERT(base - t.p[K - 1] - 1 >= 0 && base + t.p[K - 1] < tl.L && tl.L <= LSP2);
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     const float2* pl = P + base + t.p[i];
@@ -972,7 +1036,7 @@ constexpr int FPBUF = 2 * FPROD;
 #endif
 constexpr int F3PREG = SB_F3PREG, F3CREG = SB_F3CREG;
 
-template <typename Tin, int K, int MINB = 2, bool B2 = false>
+template <typename Tin, int K, int MINB = 2, bool B2 = false, int PLS = LS>
 __global__ void __launch_bounds__(FTHREADS, MINB)
     fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status,
                  const __grid_constant__ CUtensorMap omap) {
@@ -991,8 +1055,10 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
   const long long T0 = item * tl.rows_per_item;
   const long long T1 = min(T0 + tl.rows_per_item, total);
   const bool packed = (sizeof(Tin) == 1) && tl.packed;
-  constexpr int NSB = MINB == 3 ? 1 : 2;  // staged bands per producer warp
-  const int pbuf_words = packed ? HB * LSP2 : HB * LS;  // packed: HB/2 float2 rows
+  // staged bands per producer warp: one for the three-CTA uint8 kernel and the small-stride
+  // float32 kernel (two CTAs per SM), two otherwise
+  constexpr int NSB = (MINB == 3 || (!B2 && PLS == LS_SMALL && sizeof(Tin) == 4)) ? 1 : 2;
+  const int pbuf_words = packed ? HB * LSP2 : HB * PLS;  // packed: HB/2 float2 rows
   unsigned char* stage = smem;                                          // FPROD producers x NSB staged bands
   int* Pbase = (int*)(smem + NSB * FPROD * HB * tl.stage_row_bytes);    // FPROD x npb prefix buffers
   // FCONS x 2 output bands of HB x 32 floats (TMA stores; 128-byte aligned shared addresses)
@@ -1074,7 +1140,7 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
           if constexpr (sizeof(Tin) == 1)
             scan_rows<Tin>(cur, P, g, t, tl, ch, n, status, 0, 1);
           else
-            scan_band8<Tin>(cur, P, g, t, tl, ch, n, status);
+            scan_band8<Tin, PLS>(cur, P, g, t, tl, ch, n, status);
         }
         if (NSB == 1) {  // single staged band: the next one lands while the other producers' bands are used
           __syncwarp();
@@ -1135,6 +1201,7 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
           cprefix += (int)cv[r] - kMagicBits;
           cv[r] = (uint32_t)cprefix;
         }
+        SB_ASSERT(prod_slot + 2 * HB <= D && D + 2 * HB <= tl.tmem_cols);
         tmem_st32(tlane + (uint32_t)prod_slot, cv);
         if (prod_slot == 0) tmem_st32(tlane + (uint32_t)D, cv);  // 32-row mirror
         tmem_wait_st();
@@ -1150,6 +1217,7 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
             int tr = out_mod + t.pmax - t.p[i];
             l = l >= D ? l - D : l;
             tr = tr >= D ? tr - D : tr;
+            SB_ASSERT(l >= 0 && tr >= 0 && l < D && tr < D);
             uint32_t lv[2 * HB], tv[2 * HB];
             tmem_ld32(tlane + (uint32_t)l, lv);
             tmem_ld32(tlane + (uint32_t)tr, tv);
@@ -1228,7 +1296,7 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
             rv[q + HB / 2] = r2[q].y;
           }
         } else {
-          band_rows<K, LS>(P, c, t.w_row, t, tl, rv);
+          band_rows<K, PLS>(P, c, t.w_row, t, tl, rv);
 #pragma unroll
           for (int r = 0; r < HB; ++r) rv[r] += kMagic;  // round to the mid quantum
         }
@@ -1240,6 +1308,7 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
             cprefix += __float_as_int(rv[r]) - kMagicBits;
             cv[r] = (uint32_t)cprefix;
           }
+          SB_ASSERT(prod_slot + HB <= D && D + HB <= tl.tmem_cols);
           tmem_st16(tlane + (uint32_t)prod_slot, cv);
           if (prod_slot == 0) tmem_st16(tlane + (uint32_t)D, cv);  // mirror: lag windows never wrap
           tmem_wait_st();
@@ -1411,7 +1480,7 @@ __global__ void __launch_bounds__(C2THREADS, 1)
   const int D = tl.D, NB = D / HB, PF = tl.pf, DS = tl.ds;
   unsigned char* abase = smem + (((smem_u32(smem) + 127u) & ~127u) - smem_u32(smem));  // TMA: 128-byte aligned
   int* lring = (int*)abase;                   // [PF][2][HB][WS] plane band pairs (TMA tensor loads)
-  int* dring = lring + PF * 2 * HB * WS;      // [DS][HB][WS] copies of old ring bands
+  int* dring = lring + PF * 2 * HB * WS;      // [DS + 1][HB][WS] copies of old ring bands (+ mirror of slot 0)
   float* obuf = (float*)(abase + tl.obuf_off);
   if (threadIdx.x == 0) {
     for (int i = 0; i < NB; ++i) mbar_init(&full[i], 32 * 4);
@@ -1542,6 +1611,11 @@ __global__ void __launch_bounds__(C2THREADS, 1)
               int* dp = dring + dslot * (HB * WS) + c;
 #pragma unroll
               for (int r = 0; r < HB; ++r) dp[r * WS] = (int)old[d][r];
+              if (dslot == 0) {  // mirror of copy slot 0 after the last slot: trail windows never wrap
+                int* mp = dring + DS * (HB * WS) + c;
+#pragma unroll
+                for (int r = 0; r < HB; ++r) mp[r * WS] = (int)old[d][r];
+              }
               if (++dslot == DS) dslot = 0;
             }
             if (++cslot == NB) cslot = 0;
@@ -1591,6 +1665,7 @@ __global__ void __launch_bounds__(C2THREADS, 1)
           int l = base + t.pmax + 1 + t.p[i];
           l = l >= D ? l - D : l;
           l = l >= D ? l - D : l;
+          SB_ASSERT(l >= 0 && l < D);
           tmem_ld16(tlane + (uint32_t)l, lvp[d2]);
           if (!((tl.deepmask >> i) & 1)) {
             int tr = base + t.pmax - t.p[i];
@@ -1612,18 +1687,11 @@ __global__ void __launch_bounds__(C2THREADS, 1)
             const uint32_t u0 = j + (uint32_t)(off / HB);
             const int r0 = off % HB;
             const int s0 = (int)(u0 % (uint32_t)DS);
-            const int* p0 = dring + s0 * (HB * WS) + c;
-            if (r0 == 0) {
+            SB_ASSERT(DS > 0 && s0 < DS);
+            // rows s0*HB + r0 .. +15 of the linear copy ring (slot 0 is mirrored after slot DS-1)
+            const int* p0 = dring + (s0 * HB + r0) * WS + c;
 #pragma unroll
-              for (int r = 0; r < HB; ++r) tv[r] = (uint32_t)p0[r * WS];
-            } else {
-              const int* p1 = dring + (s0 + 1 == DS ? 0 : s0 + 1) * (HB * WS) + c;
-#pragma unroll
-              for (int r = 0; r < HB; ++r) {
-                const int rr = r0 + r;
-                tv[r] = (uint32_t)(rr < HB ? p0[rr * WS] : p1[(rr - HB) * WS]);
-              }
-            }
+            for (int r = 0; r < HB; ++r) tv[r] = (uint32_t)p0[r * WS];
           }
           const float2 w2 = make_float2(t.w_col[i], t.w_col[i]);
 #pragma unroll
@@ -1767,7 +1835,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
       // CH-column chunks; the row's running prefix (carry) lives in the 4 lanes of that row
       int carry = 0;
       issue(0, 0);
-      uint32_t bad = 0;
+      RangeAcc bad;
       for (int j = 0; j < nin; ++j) {
         const uint32_t gj = cin_ctr + j;
         cp_async_wait_all();
@@ -1804,7 +1872,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
         }
         mbar_arrive(&bar_full[gj % NSLOT]);
       }
-      report_status(status, bad);
+      report_status(status, bad, t);
     } else {
       const int c = threadIdx.x;
       int* midrow[HB];  // destination rows of this band - hoisted
@@ -1903,6 +1971,7 @@ const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)
 const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
 const void* sweep_ptr_fused5(int k);      // fused sweep, two bands per consumer iteration (uint8, one channel)
+const void* sweep_ptr_fused_f32(int k, int ls);  // fused sweep of float32 sources with prefix stride ls
 
 template <typename Tin>
 const void* sweep_ptr_for(Mode m, int k) {
@@ -1930,6 +1999,13 @@ const void* sweep_ptr_for(Mode m, int k) {
 #undef SB_FUSED
 #undef SB_ROWS_MID
 #undef SB_ROWS_OUT
+}
+
+template <int PLS>
+inline const void* fused_f32_ptr_for(int k) {
+#define SB_FF(KK) fused_kernel<float, KK, 2, false, PLS>
+  SB_K_CASES(SB_FF)
+#undef SB_FF
 }
 
 inline const void* cols_ptr_for(int k) {
