@@ -334,6 +334,72 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
   return false;
 }
 
+// Tiling of the wide fused sweep (sweep_wide.cu): staged / prefix rows of L columns in
+// slots of WLS words, the cols2_kernel ring (496 rows of TMEM, trails older than the ring
+// from shared-memory band copies, lag / copy_e / ds / deepmask as in cols_prefix_tiling with
+// WCG output groups) and tl.pf = the number of producer slots that fit shared memory.
+// False when no slot stride bounds L, a window would straddle ring and copies, or the
+// buffers do not fit (the two-launch path runs then).
+constexpr size_t kWideSmem = 226 * 1024;  // one CTA per SM (static shared memory is < 1 KB)
+
+bool fusedw_tiling(const int64_t* radii, int k, int pmax, sb::Tiling* out) {
+  sb::Tiling tl;
+  std::memset(&tl, 0, sizeof(tl));
+  tl.xoff = ceil16(pmax + 1);
+  tl.sw = sb::WS;
+  tl.L = ceil16(tl.xoff + sb::WS + pmax);
+  int lsw = 0;
+  for (int b : sb::WLS)
+    if (b >= tl.L) {
+      lsw = b;
+      break;
+    }
+  if (!lsw) return false;
+  tl.ls = lsw;
+  tl.stage_row_bytes = lsw * 4;
+  const int NB = 31;
+  tl.D = NB * sb::HB;
+  tl.tmem_cols = 512;
+  const size_t band = (size_t)sb::HB * sb::WS * sizeof(int);
+  const size_t slot = (size_t)sb::HB * lsw * sizeof(int);
+  const size_t obuf = (size_t)4 * sb::WCG * 2 * sb::HB * 32 * sizeof(float) + 128;
+  const int span = 2 + pmax / 8;  // ring bands one output band reads
+  const int slack0 = NB - span - sb::WCG + 1 < 0 ? 3 : NB - span - sb::WCG + 1;
+  // the most slack (row warps running ahead of the output groups) that leaves room for
+  // three producer slots; two slots only when nothing else fits
+  for (int it = 0; it < 2 * (slack0 + 1); ++it) {
+    const int min_fp = it <= slack0 ? 3 : 2;
+    const int slack = slack0 - (it % (slack0 + 1));
+    tl.lag = span + sb::WCG - 1 + slack;
+    tl.copy_e = tl.lag - span + 1;
+    if (tl.lag - span + 1 > sb::C2DONE) continue;
+    const int thr = tl.lag - 1 - NB;  // bands at offset <= thr come from the copies
+    tl.deepmask = 0;
+    bool ok = true;
+    for (int i = 0; i < k && ok; ++i) {
+      const int off = pmax - (int)radii[i];
+      const int lo = off / sb::HB, hi = (off + sb::HB - 1) / sb::HB;
+      if (hi <= thr) tl.deepmask |= 1 << i;
+      else if (lo <= thr) ok = false;
+      if ((pmax + 1 + (int)radii[i]) / sb::HB <= thr) ok = false;
+    }
+    if (!ok) continue;
+    tl.ds = thr >= 0 ? 2 * tl.lag - NB - span + 2 : 0;
+    const int copies = tl.ds ? tl.ds + 1 : 0;
+    tl.pf = 0;
+    for (int fp = sb::WPROD; fp >= min_fp; --fp)
+      if (fp * slot + (size_t)copies * band + obuf <= kWideSmem) {
+        tl.pf = fp;
+        break;
+      }
+    if (!tl.pf) continue;
+    tl.obuf_off = (int)((size_t)tl.pf * slot + (size_t)copies * band);
+    *out = tl;
+    return true;
+  }
+  return false;
+}
+
 // Immutable launch facts, looked up once per (kernel, device) instead of on every call
 // (small images are host-bound otherwise): register count, static shared memory, the
 // dynamic shared memory already granted with cudaFuncSetAttribute, and the device's SM
@@ -527,7 +593,7 @@ int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, c
 // ---------------------------------------------------------------- path choice
 // One decision shared by the workspace queries and the launches (so a caller that
 // sized its workspace with the query always has enough).
-enum class RowPath { Fused, Stream, Tiled, Generic };
+enum class RowPath { Fused, FusedWide, Stream, Tiled, Generic };
 enum class ColPath { None, Prefix, Running, Generic };
 
 struct Route {
@@ -566,6 +632,13 @@ Route route_2d(int src_dtype, int64_t width, int channels, const int64_t* radii,
   const bool fast = k <= sb::FAST_K && g_policy != SB_PATH_GENERIC && !r.wide;
   if (fast && g_policy != SB_PATH_UNFUSED && fused_fits(pmax, channels, es)) {
     r.rows = RowPath::Fused;
+    r.cols = ColPath::None;
+    return r;
+  }
+  sb::Tiling wt;
+  if (fast && g_policy == SB_PATH_FUSED_WIDE && src_dtype == SB_DTYPE_F32 && channels == 1 &&
+      fusedw_tiling(radii, k, pmax, &wt)) {
+    r.rows = RowPath::FusedWide;
     r.cols = ColPath::None;
     return r;
   }
@@ -611,7 +684,7 @@ extern "C" {
 int sb_version(void) { return 4; }
 
 int sb_set_path_policy(int policy) {
-  if (policy < SB_PATH_AUTO || policy > SB_PATH_U8_ONE_BAND) return -1;
+  if (policy < SB_PATH_AUTO || policy > SB_PATH_FUSED_WIDE) return -1;
   const int prev = g_policy;
   g_policy = policy;
   return prev;
@@ -668,7 +741,7 @@ size_t sb_separable_filter_2d_workspace_bytes(int src_dtype, int64_t batch, int6
   if (!radii || k < 1 || k > SB_MAX_K || batch < 1 || height < 1 || width < 1 || channels < 1) return 0;
   if (dtype_size(src_dtype) == 0 || radii[k - 1] < 0 || radii[k - 1] > 0x7fffffff) return 0;
   const Route r = route_2d(src_dtype, width, channels, radii, k);
-  if (r.rows == RowPath::Fused) return 0;
+  if (r.rows == RowPath::Fused || r.rows == RowPath::FusedWide) return 0;
   const size_t plane = (size_t)batch * height * width * channels * (r.wide ? sizeof(long long) : sizeof(int));
   return r.scratch_bytes ? align256(plane) + r.scratch_bytes : plane;
 }
@@ -731,6 +804,46 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     rc = plan_launch(fn, sb::Mode::Fused, base, plan.pmax, g.W, total_rows, channels, &L);
     if (rc) return rc;
     return launch_fused(fn, L, src, dst, g, plan.taps, status_dev, st);
+  }
+  if (route.rows == RowPath::FusedWide) {
+    sb::Tiling tl;
+    if (!fusedw_tiling(radii, k, plan.pmax, &tl)) return fail(SB_ERR_INVALID_ARGUMENT, "wide sweep tiling");
+    tl.nstrips = (g.W + sb::WS - 1) / sb::WS;
+    const void* fn = sb::sweep_ptr_fusedw(k, tl.ls);
+    const size_t smem = (size_t)tl.obuf_off + 128 + (size_t)4 * sb::WCG * 2 * sb::HB * 32 * sizeof(float);
+    FnFacts ff;
+    DevFacts df;
+    rc = launch_facts(fn, smem, &ff, &df);
+    if (rc) return rc;
+    // persistent: one CTA per SM over (row chunk, strip) units taken round-robin; the chunk
+    // height minimises (rounds of units) x (chunk rows + the 2*pmax+1 warm-up rows)
+    const long long warm = 2LL * plan.pmax + 1 + sb::HB;
+    long long best_chunks = 1;
+    double best_cost = 1e300;
+    for (long long nc = 1; nc <= 64 && nc <= std::max(1LL, total_rows / sb::HB); ++nc) {
+      const long long units = nc * tl.nstrips;
+      const long long rounds = (units + df.sms - 1) / df.sms;
+      const double cost = (double)rounds * (double)((total_rows + nc - 1) / nc + warm);
+      if (cost < best_cost * 0.995) {
+        best_cost = cost;
+        best_chunks = nc;
+      }
+    }
+    tl.rows_per_item = (total_rows + best_chunks - 1) / best_chunks;
+    const long long units = ((total_rows + tl.rows_per_item - 1) / tl.rows_per_item) * tl.nstrips;
+    const long long grid = std::min<long long>(df.sms, units);
+    sb::Geometry gw = g;
+    alignas(64) CUtensorMap omap;
+    make_output_map(dst, gw, &omap);
+    if (debug_plans())
+      std::fprintf(stderr, "[sliceblur_b200] wide fused: pmax=%d L=%d ls=%d fp=%d ds=%d lag=%d deep=%x smem=%zu grid=%lld "
+                   "chunk=%lld units=%lld\n",
+                   plan.pmax, tl.L, tl.ls, tl.pf, tl.ds, tl.lag, tl.deepmask, smem, grid, tl.rows_per_item, units);
+    void* args[] = {(void*)&src, (void*)&dst, (void*)&gw, (void*)&plan.taps, (void*)&tl, (void*)&status_dev,
+                    (void*)&omap};
+    cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(sb::WTHREADS), args, smem, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+    return SB_OK;
   }
   // two passes through an int32 workspace laid out [channel][batch][H][W]
   const size_t need = sb_separable_filter_2d_workspace_bytes(src_dtype, batch, height, width, channels, radii, k);

@@ -1457,6 +1457,14 @@ constexpr int C2THREADS = 32 * 4 * (1 + CG);   // loader group + CG output group
 constexpr int C2DONE = 32;  // output-band done barriers: >= lag - span + 1, so no barrier is lapped
 constexpr int C2PF = 8;     // max plane-band slots (TMA ring)
 
+// Wide fused sweep (sweep_wide.cu): float32, one channel, radii past fused_kernel's reach.
+// 4 row warps + WCG output groups of 4 warps + WPROD producer warps; slot row strides WLS
+// (words, = 4 mod 32 so rows are 16 mod 128 bytes apart) bound the staged row length L.
+constexpr int WCG = 2;
+constexpr int WPROD = 4;
+constexpr int WTHREADS = 32 * (4 + 4 * WCG + WPROD);
+constexpr int WLS[3] = {516, 676, 900};
+
 template <int K>
 __global__ void __launch_bounds__(C2THREADS, 1)
     cols2_kernel(const int* __restrict__ mid_in, float* __restrict__ dst, Geometry g, Taps t, Tiling tl,
@@ -1972,6 +1980,7 @@ const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources
 const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
 const void* sweep_ptr_fused5(int k);      // fused sweep, two bands per consumer iteration (uint8, one channel)
 const void* sweep_ptr_fused_f32(int k, int ls);  // fused sweep of float32 sources with prefix stride ls
+const void* sweep_ptr_fusedw(int k, int lsw);    // wide fused sweep (sweep_wide.cu), slot stride lsw
 
 template <typename Tin>
 const void* sweep_ptr_for(Mode m, int k) {
