@@ -61,9 +61,11 @@ enum {
   SB_PATH_UNFUSED = 2,      /* row pass to an int32 plane, then a column kernel (no fused sweep)     */
   SB_PATH_U8_THREE_CTA = 3, /* uint8 fused sweep: three CTAs per SM, one band per consumer turn     */
   SB_PATH_U8_ONE_BAND = 4,  /* uint8 fused sweep: two CTAs per SM, one band per consumer turn       */
-  SB_PATH_FUSED_WIDE = 5    /* float32 one-channel, radii past the fused sweep: one launch, the row
+  SB_PATH_FUSED_WIDE = 5,   /* float32 one-channel, radii past the fused sweep: one launch, the row
                                values never in HBM (DRAM 1.05x algorithmic; slower than the default
                                two-launch path at these radii); else as AUTO          */
+  SB_PATH_U8_ROWTILE = 6    /* uint8 one-channel, small radii: the row-tile sweep (row pass on
+                               thread-per-row warps with the row prefix in TMEM); else as AUTO      */
 };
 
 /* return codes */

@@ -36,6 +36,7 @@ SB_PATH_UNFUSED = 2
 SB_PATH_U8_THREE_CTA = 3
 SB_PATH_U8_ONE_BAND = 4
 SB_PATH_FUSED_WIDE = 5
+SB_PATH_U8_ROWTILE = 6
 
 #: Every symbol include/sliceblur_b200.h declares (tests check the exports).
 EXPORTED_SYMBOLS = (

@@ -400,6 +400,50 @@ bool fusedw_tiling(const int64_t* radii, int k, int pmax, sb::Tiling* out) {
   return false;
 }
 
+// Tiling of the uint8 row-tile sweep (sweep_rowtile.cu): staged rows [xb, xb + L) with
+// xb = x0 - xoff (16-byte aligned), TMEM row-prefix region of ta columns from staged column
+// s0, a ring of D rows (32-row slots) plus its 32-row mirror behind it, all in one 512-column
+// allocation (one CTA per SM).  False when the radii do not fit.
+bool rowtile_tiling(int pmax, sb::Tiling* out) {
+  sb::Tiling tl;
+  std::memset(&tl, 0, sizeof(tl));
+  tl.xoff = ceil16(pmax + 1);
+  tl.sw = sb::WS;
+  tl.L = ceil16(tl.xoff + sb::WS + pmax);
+  tl.stage_row_bytes = (tl.L / 16) % 2 ? tl.L : tl.L + 16;  // odd multiple of 16: conflict-free
+  tl.s0 = (tl.xoff - pmax - 1) & ~7;  // 8-byte aligned (the scan combines 16-byte halves)
+  tl.ta = ceil16(tl.xoff + sb::WS + pmax - tl.s0);
+  tl.D = sb::TB * ((2 * pmax + 2 * sb::TB + 1 + sb::TB - 1) / sb::TB);
+  tl.tmem_cols = 512;
+  // two row-prefix regions (two row warps per lane quadrant), the ring and its 32-row mirror
+  if (2 * tl.ta + tl.D + sb::TB > 512 || tl.D / sb::TB > 16) return false;
+  if ((tl.s0 & 15) && ceil16(tl.s0) + tl.ta + 16 > tl.L + 16) return false;  // the scan reads one chunk ahead
+  const size_t stage = (size_t)sb::TROWW * sb::TB * tl.stage_row_bytes;
+  const size_t slots = (size_t)sb::TRS * sb::TB * sb::TRSW * sizeof(float);
+  tl.obuf_off = (int)(((stage + slots) + 127) & ~(size_t)127);
+  const size_t smem = (size_t)tl.obuf_off + 128 + (size_t)4 * sb::TOG * 2 * sb::TB * 32 * sizeof(float);
+  if (smem > 226 * 1024) return false;
+  *out = tl;
+  return true;
+}
+
+// Persistent (row chunk, strip) units over `sms` CTAs: the chunk count minimising
+// (rounds of units) x (chunk rows + warm-up rows).  Returns the chunk height.
+long long persistent_chunk(long long total_rows, int nstrips, int sms, long long warm, int band) {
+  long long best_chunks = 1;
+  double best_cost = 1e300;
+  for (long long nc = 1; nc <= 512 && nc <= std::max(1LL, total_rows / band); ++nc) {
+    const long long units = nc * nstrips;
+    const long long rounds = (units + sms - 1) / sms;
+    const double cost = (double)rounds * (double)((total_rows + nc - 1) / nc + warm);
+    if (cost < best_cost * 0.995) {
+      best_cost = cost;
+      best_chunks = nc;
+    }
+  }
+  return (total_rows + best_chunks - 1) / best_chunks;
+}
+
 // Immutable launch facts, looked up once per (kernel, device) instead of on every call
 // (small images are host-bound otherwise): register count, static shared memory, the
 // dynamic shared memory already granted with cudaFuncSetAttribute, and the device's SM
@@ -593,7 +637,7 @@ int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, c
 // ---------------------------------------------------------------- path choice
 // One decision shared by the workspace queries and the launches (so a caller that
 // sized its workspace with the query always has enough).
-enum class RowPath { Fused, FusedWide, Stream, Tiled, Generic };
+enum class RowPath { Fused, FusedWide, RowTile, Stream, Tiled, Generic };
 enum class ColPath { None, Prefix, Running, Generic };
 
 struct Route {
@@ -630,6 +674,13 @@ Route route_2d(int src_dtype, int64_t width, int channels, const int64_t* radii,
   Route r{RowPath::Generic, ColPath::Generic, needs_wide(pmax), 0};
   const int es = dtype_size(src_dtype);
   const bool fast = k <= sb::FAST_K && g_policy != SB_PATH_GENERIC && !r.wide;
+  sb::Tiling rt;
+  if (fast && g_policy == SB_PATH_U8_ROWTILE && src_dtype == SB_DTYPE_U8 && channels == 1 &&
+      rowtile_tiling(pmax, &rt)) {
+    r.rows = RowPath::RowTile;
+    r.cols = ColPath::None;
+    return r;
+  }
   if (fast && g_policy != SB_PATH_UNFUSED && fused_fits(pmax, channels, es)) {
     r.rows = RowPath::Fused;
     r.cols = ColPath::None;
@@ -684,7 +735,7 @@ extern "C" {
 int sb_version(void) { return 4; }
 
 int sb_set_path_policy(int policy) {
-  if (policy < SB_PATH_AUTO || policy > SB_PATH_FUSED_WIDE) return -1;
+  if (policy < SB_PATH_AUTO || policy > SB_PATH_U8_ROWTILE) return -1;
   const int prev = g_policy;
   g_policy = policy;
   return prev;
@@ -741,7 +792,7 @@ size_t sb_separable_filter_2d_workspace_bytes(int src_dtype, int64_t batch, int6
   if (!radii || k < 1 || k > SB_MAX_K || batch < 1 || height < 1 || width < 1 || channels < 1) return 0;
   if (dtype_size(src_dtype) == 0 || radii[k - 1] < 0 || radii[k - 1] > 0x7fffffff) return 0;
   const Route r = route_2d(src_dtype, width, channels, radii, k);
-  if (r.rows == RowPath::Fused || r.rows == RowPath::FusedWide) return 0;
+  if (r.rows == RowPath::Fused || r.rows == RowPath::FusedWide || r.rows == RowPath::RowTile) return 0;
   const size_t plane = (size_t)batch * height * width * channels * (r.wide ? sizeof(long long) : sizeof(int));
   return r.scratch_bytes ? align256(plane) + r.scratch_bytes : plane;
 }
@@ -804,6 +855,30 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     rc = plan_launch(fn, sb::Mode::Fused, base, plan.pmax, g.W, total_rows, channels, &L);
     if (rc) return rc;
     return launch_fused(fn, L, src, dst, g, plan.taps, status_dev, st);
+  }
+  if (route.rows == RowPath::RowTile) {
+    sb::Tiling tl;
+    if (!rowtile_tiling(plan.pmax, &tl)) return fail(SB_ERR_INVALID_ARGUMENT, "row-tile tiling");
+    tl.nstrips = (g.W + sb::WS - 1) / sb::WS;
+    const void* fn = sb::sweep_ptr_rowtile(k);
+    const size_t smem = (size_t)tl.obuf_off + 128 + (size_t)4 * sb::TOG * 2 * sb::TB * 32 * sizeof(float);
+    FnFacts ff;
+    DevFacts df;
+    rc = launch_facts(fn, smem, &ff, &df);
+    if (rc) return rc;
+    tl.rows_per_item = persistent_chunk(total_rows, tl.nstrips, df.sms, 2LL * plan.pmax + 1 + sb::TB, sb::TB);
+    const long long units = ((total_rows + tl.rows_per_item - 1) / tl.rows_per_item) * tl.nstrips;
+    const long long grid = std::min<long long>(df.sms, units);
+    sb::Geometry gr = g;
+    alignas(64) CUtensorMap omap;
+    make_output_map(dst, gr, &omap);
+    if (debug_plans())
+      std::fprintf(stderr, "[sliceblur_b200] row-tile: pmax=%d L=%d srb=%d s0=%d ta=%d D=%d smem=%zu grid=%lld chunk=%lld units=%lld\n",
+                   plan.pmax, tl.L, tl.stage_row_bytes, tl.s0, tl.ta, tl.D, smem, grid, tl.rows_per_item, units);
+    void* args[] = {(void*)&src, (void*)&dst, (void*)&gr, (void*)&plan.taps, (void*)&tl, (void*)&omap};
+    cudaError_t e = cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(sb::TTHREADS), args, smem, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+    return SB_OK;
   }
   if (route.rows == RowPath::FusedWide) {
     sb::Tiling tl;

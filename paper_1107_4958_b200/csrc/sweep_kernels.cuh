@@ -118,6 +118,8 @@ struct Tiling {
   int copy_e;           // cols2: band v - D/HB + copy_e is copied out of the ring while band v is written
   int split;            // fused: 3 = three-CTA-per-SM variant (fused_kernel<uint8_t, K, 3>)
   int nsb;              // fused: staged bands per producer warp (1 or 2; the output box is buffered alike)
+  int s0;               // row-tile: first scanned staged column (multiple of 4)
+  int ta;               // row-tile: TMEM columns of the row-prefix region (the ring follows)
 };
 
 enum class Mode : int { Fused = 0, RowsToMid = 1, RowsToOut = 2, ColsFromMid = 3, ColsPrefix = 4 };
@@ -1457,6 +1459,54 @@ constexpr int C2THREADS = 32 * 4 * (1 + CG);   // loader group + CG output group
 constexpr int C2DONE = 32;  // output-band done barriers: >= lag - span + 1, so no barrier is lapped
 constexpr int C2PF = 8;     // max plane-band slots (TMA ring)
 
+// Work units: unit u = (row chunk u / nstrips, strip u % nstrips) covers tall rows
+// [rc * Hc, min((rc + 1) * Hc, total)) of one 128-column strip (the tall image stacks the
+// batch; Hc = tl.rows_per_item).  CTA b takes units b, b + grid, ... so the CTAs running at
+// any moment sweep neighbouring strips over the same rows and every strip's halo columns
+// are L2 hits.  A unit splits into segments at image boundaries; every segment restarts
+// the sweep (virtual rows a-1-pmax .. b-1+pmax of the output rows [a, b)); gb0 is the
+// CTA-global index of the segment's first band (bands of bh rows).
+struct WorkIter {
+  long long T, Tend, total, wh, Hc;
+  int u, nunits, nstrips, oy0, pmax, bh;
+  int strip, img, a, b, count, nbands;
+  uint32_t gb0;
+  bool valid;
+  __device__ __forceinline__ void init(long long total_, long long Hc_, int nstrips_, long long wh_, int oy0_,
+                                       int pmax_, int bh_ = HB) {
+    total = total_, Hc = Hc_, nstrips = nstrips_, wh = wh_, oy0 = oy0_, pmax = pmax_, bh = bh_, gb0 = 0, nbands = 0;
+    nunits = (int)((total + Hc - 1) / Hc) * nstrips;
+    u = blockIdx.x;
+    load_unit();
+  }
+  __device__ __forceinline__ void load_unit() {
+    valid = u < nunits;
+    if (!valid) return;
+    strip = u % nstrips;
+    T = (long long)(u / nstrips) * Hc;
+    Tend = min(T + Hc, total);
+    load();
+  }
+  __device__ __forceinline__ void load() {
+    img = (int)(T / wh);
+    const long long r = T - (long long)img * wh;
+    a = oy0 + (int)r;
+    b = oy0 + (int)min(wh, r + (Tend - T));
+    count = (b - a) + 2 * pmax + 1;
+    nbands = (count + bh - 1) / bh;
+  }
+  __device__ __forceinline__ void next() {
+    T += (long long)(b - a);
+    gb0 += (uint32_t)nbands;
+    if (T < Tend) {
+      load();
+    } else {
+      u += gridDim.x;
+      load_unit();
+    }
+  }
+};
+
 // Wide fused sweep (sweep_wide.cu): float32, one channel, radii past fused_kernel's reach.
 // 4 row warps + WCG output groups of 4 warps + WPROD producer warps; slot row strides WLS
 // (words, = 4 mod 32 so rows are 16 mod 128 bytes apart) bound the staged row length L.
@@ -1464,6 +1514,26 @@ constexpr int WCG = 2;
 constexpr int WPROD = 4;
 constexpr int WTHREADS = 32 * (4 + 4 * WCG + WPROD);
 constexpr int WLS[3] = {516, 676, 900};
+
+// Row-tile sweep (sweep_rowtile.cu): uint8, one channel, small radii.  32-row bands; 8 row
+// warps (thread = row; two per TMEM lane quadrant), 4 loader warps and TOG output groups of 4
+// (thread = column); TRS row-value slots of TB rows x TRSW words (528 B = 16 mod 128).
+#ifndef SB_TOG
+#define SB_TOG 2
+#endif
+#ifndef SB_TROWW
+#define SB_TROWW 8
+#endif
+#ifndef SB_TRS
+#define SB_TRS 4
+#endif
+constexpr int TB = 32;
+constexpr int TOG = SB_TOG;
+constexpr int TROWW = SB_TROWW;
+constexpr int TTHREADS = 32 * (TROWW + 4 + 4 * TOG);
+constexpr int TRS = SB_TRS;
+constexpr int TRSW = WS + 4;
+constexpr int TDONE = 32;  // output-band done barriers
 
 template <int K>
 __global__ void __launch_bounds__(C2THREADS, 1)
@@ -1981,6 +2051,7 @@ const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uin
 const void* sweep_ptr_fused5(int k);      // fused sweep, two bands per consumer iteration (uint8, one channel)
 const void* sweep_ptr_fused_f32(int k, int ls);  // fused sweep of float32 sources with prefix stride ls
 const void* sweep_ptr_fusedw(int k, int lsw);    // wide fused sweep (sweep_wide.cu), slot stride lsw
+const void* sweep_ptr_rowtile(int k);            // uint8 row-tile sweep (sweep_rowtile.cu)
 
 template <typename Tin>
 const void* sweep_ptr_for(Mode m, int k) {

@@ -34,54 +34,6 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
                : "memory");
 }
 
-// Work units: unit u = (row chunk u / nstrips, strip u % nstrips) covers tall rows
-// [rc * Hc, min((rc + 1) * Hc, total)) of one 128-column strip (the tall image stacks the
-// batch; Hc = tl.rows_per_item).  CTA b takes units b, b + grid, ... so the CTAs running at
-// any moment sweep neighbouring strips over the same rows and every strip's halo columns
-// are L2 hits.  A unit splits into segments at image boundaries; every segment restarts
-// the sweep (virtual rows a-1-pmax .. b-1+pmax of the output rows [a, b)); gb0 is the
-// CTA-global index of the segment's first band.
-struct WorkIter {
-  long long T, Tend, total, wh, Hc;
-  int u, nunits, nstrips, oy0, pmax;
-  int strip, img, a, b, count, nbands;
-  uint32_t gb0;
-  bool valid;
-  __device__ __forceinline__ void init(long long total_, long long Hc_, int nstrips_, long long wh_, int oy0_,
-                                       int pmax_) {
-    total = total_, Hc = Hc_, nstrips = nstrips_, wh = wh_, oy0 = oy0_, pmax = pmax_, gb0 = 0, nbands = 0;
-    nunits = (int)((total + Hc - 1) / Hc) * nstrips;
-    u = blockIdx.x;
-    load_unit();
-  }
-  __device__ __forceinline__ void load_unit() {
-    valid = u < nunits;
-    if (!valid) return;
-    strip = u % nstrips;
-    T = (long long)(u / nstrips) * Hc;
-    Tend = min(T + Hc, total);
-    load();
-  }
-  __device__ __forceinline__ void load() {
-    img = (int)(T / wh);
-    const long long r = T - (long long)img * wh;
-    a = oy0 + (int)r;
-    b = oy0 + (int)min(wh, r + (Tend - T));
-    count = (b - a) + 2 * pmax + 1;
-    nbands = (count + HB - 1) / HB;
-  }
-  __device__ __forceinline__ void next() {
-    T += (long long)(b - a);
-    gb0 += (uint32_t)nbands;
-    if (T < Tend) {
-      load();
-    } else {
-      u += gridDim.x;
-      load_unit();
-    }
-  }
-};
-
 // In-place prefix scan of rows r0 .. r0+3 (those < n) of a slot: float32 elements ->
 // inclusive int32 prefixes in the input quantum (to_fixed).  Lane (rr, cq) = (lane & 3,
 // lane >> 2) takes chunk cg + cq of row r0 + rr, so each 8-lane phase of the 128-bit

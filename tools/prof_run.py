@@ -15,6 +15,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+from paper_1107_4958_b200 import _native as nat  # noqa: E402
 from paper_1107_4958_b200 import filtering, table_kernel  # noqa: E402
 
 
@@ -22,7 +23,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c3", choices=sorted(bench.CONFIGS))
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--policy", type=int, default=0, help="sb_set_path_policy value (SB_PATH_*)")
     args = ap.parse_args()
+    nat.path_policy(args.policy).__enter__()
     cfg = bench.CONFIGS[args.config]
     dev = torch.device("cuda", 0)
     x = bench.make_inputs(cfg, 1000, dev)
