@@ -1721,8 +1721,18 @@ __global__ void __launch_bounds__(C2THREADS, 1)
         const int nb = min(HB, so.b - out_next);
         const uint32_t j = so.gb0 + (uint32_t)ob;  // ring band of the band's deepest trail row
         const uint32_t need = so.gb0 + (uint32_t)((ob * HB + nb + 2 * t.pmax) / HB);
+        // in order (a group's first band may need a band more than a ring ahead, so phases are
+        // observed one by one).  Without band copies (ring only, e.g. C4) the groups back off so
+        // their polling leaves issue slots to the loader (C4 1.231 -> 1.184 ms); with copies (C5)
+        // the ring is tight and the loader waits on the groups, so they spin (4.49 vs 4.54 ms).
+        const bool backoff = DS == 0;
         while (ready <= need) {
-          mbar_wait(&full[rslot], rph);
+          if (backoff) {
+            for (unsigned ns = 32; !mbar_test(&full[rslot], rph); ns = ns < 256 ? 2 * ns : ns) __nanosleep(ns);
+            sb_perturb();
+          } else {
+            mbar_wait(&full[rslot], rph);
+          }
           if (++rslot == NB) {
             rslot = 0;
             rph ^= 1;
