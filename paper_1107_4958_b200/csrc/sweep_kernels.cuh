@@ -1,4 +1,4 @@
-// sweep_kernels.cuh - sm_100a kernels of the running-sum Gaussian filter.
+// sweep_kernels.cuh - sm_100a kernels of the running-sum Gaussian filter (shared header).
 //
 // Reference arithmetic (filtering.py:48-64, `_filter_rows`):
 //     out[x] = sum_i w_i * (I(x + p_i) - I(x - p_i - 1))
@@ -6,32 +6,33 @@
 // I (filtering.py:10-13), i.e. out[x] = sum_i w_i * sum_{|t|<=p_i} f(clamp(x+t)).
 // separable_filter_2d (filtering.py:76-104) runs it over rows, then columns.
 //
-// B200 formulation (DESIGN.md has the derivation and the error bound):
-//   * every value entering a running sum is an int32 fixed-point number, so
-//     box sums are EXACT (two's-complement wraparound keeps prefix differences
-//     exact even when a prefix overflows);
-//   * a CTA (128 threads) owns a strip of WS=128 columns of the (batch x H)
-//     "tall" image and walks down a contiguous range of its rows;
-//   * pass 1 (rows), per band of HB=16 rows: the input segment
-//     [xb, xb+L) (xb = x0-pmax-1 rounded down to 16 px) is staged with
-//     cp.async into a double buffer one band ahead; edge strips replicate the
-//     border columns in place; each staged row is prefix-scanned by a warp
-//     (16-px chunks per lane, shuffle scan of chunk totals).  For uint8 input
-//     with small radii two rows share one 32-bit word (15-bit modular prefix
-//     fields, guard bits 15/31), halving the lagged shared-memory reads;
-//     thread c then forms R = sum_i w_i (P[c+p_i] - P[c-p_i-1]) rounded to the
-//     mid quantum (fp32 magic-number rounding, no F2I);
-//   * pass 2 (columns), fused: R goes to a shared-memory ring of D rows whose
-//     first HB rows are mirrored after the end, so every HB-row window of any
-//     lag is contiguous (immediate offsets, no wrap arithmetic); thread c keeps
-//     k exact int32 box sums, B_i += R[y+p_i] - R[y-p_i-1], and writes
-//     sum_i (w_i 2^-s_mid) float(B_i);
-//   * large radii (ring does not fit): RowsToMid writes the int32 R plane,
-//     ColsFromMid runs the column sweep reading lagged rows from L2/HBM.
+// B200 formulation (DESIGN.md "Arithmetic" has the derivation and the error bound):
+//   * every value entering a running sum is an int32 fixed-point number, so box sums are
+//     EXACT (two's-complement wraparound keeps prefix differences exact);
+//   * the column pass keeps the running column PREFIX C of the rounded row values in a ring
+//     in tensor memory (thread / column c <-> TMEM lane c, ring row <-> TMEM column, first
+//     band mirrored after the end so every window is contiguous) and every output box sum is
+//     C(y+p) - C(y-p-1): two tcgen05.ld windows, no running state;
+//   * full output bands leave by TMA tensor stores.
 //
-// Vertical replicate boundary: R of a virtual row v outside [0,H) is R of row
-// clamp(v) (the reference's column pass clamps the row-filtered image), so
-// the sweep stages clamped input rows.
+// Kernels in this header (instantiated per source type in sweep_<dtype>.cu):
+//   fused_kernel        one launch: producer warps stage (cp.async) and prefix-scan 16-row
+//                       bands of a 128-column strip into shared memory, consumer warps form the
+//                       row values, the TMEM column ring and the outputs (uint8: biased-fp32
+//                       prefixes, IDP4A scans, FADD2/FFMA2 on row pairs, two bands per turn)
+//   stream_rows_kernel  two-launch row pass (float32): full-width 16-row bands streamed in
+//                       128-column chunks with the row prefix carried in a ring -> int32 plane
+//   cols2_kernel        two-launch column pass: TMA loads of plane bands, loader warps append
+//                       the column prefix to the TMEM ring, output groups read windows; trails
+//                       older than the ring come from shared-memory band copies
+//   cols_kernel         running-sum column pass (fallback when no tensor map fits)
+//   rows_kernel         tiled row pass (other source types, row pass alone)
+// and, in their own translation units: sweep_wide.cu (fusedw_kernel, one-launch float32 for
+// large radii), sweep_rowtile.cu (rowtile_kernel, uint8 row pass on thread-per-row warps
+// with the row prefix in TMEM), generic_kernels.cu (any radius / k, int64 when needed).
+//
+// Vertical replicate boundary: R of a virtual row v outside [0,H) is R of row clamp(v) (the
+// reference's column pass clamps the row-filtered image), so the sweeps stage clamped rows.
 #pragma once
 
 #include <cstdint>
