@@ -39,6 +39,10 @@ CASES = [
     ("u16 tiled rows + cols kernels", nat.SB_PATH_UNFUSED, np.uint16, (2, 200, 150), 4, 8.0),
     ("f64 fused", nat.SB_PATH_AUTO, np.float64, (1, 96, 130), 5, 8.0),
     ("generic rows + cols", nat.SB_PATH_GENERIC, np.float32, (2, 150, 170, 3), 4, 20.0),
+    ("f32 wide fused, band copies (p_max 257)", nat.SB_PATH_FUSED_WIDE, np.float32, (1, 700, 600), 4, 100.0),
+    ("f32 wide fused, batch, odd width", nat.SB_PATH_FUSED_WIDE, np.float32, (3, 400, 517), 4, 40.0),
+    ("u8 row-tile", nat.SB_PATH_U8_ROWTILE, np.uint8, (9, 300, 1000), 3, 10.0),
+    ("u8 row-tile, tiny images", nat.SB_PATH_U8_ROWTILE, np.uint8, (61, 37, 150), 3, 3.0),
 ]
 
 
