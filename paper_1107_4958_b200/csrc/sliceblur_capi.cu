@@ -421,7 +421,7 @@ bool rowtile_tiling(int pmax, sb::Tiling* out) {
   const size_t stage = (size_t)sb::TROWW * sb::TB * tl.stage_row_bytes;
   const size_t slots = (size_t)sb::TRS * sb::TB * sb::TRSW * sizeof(float);
   tl.obuf_off = (int)(((stage + slots) + 127) & ~(size_t)127);
-  const size_t smem = (size_t)tl.obuf_off + 128 + (size_t)4 * sb::TOG * 2 * sb::TB * 32 * sizeof(float);
+  const size_t smem = (size_t)tl.obuf_off + 128 + (size_t)4 * sb::TOG * sb::TOBUF * sb::TB * 32 * sizeof(float);
   if (smem > 226 * 1024) return false;
   *out = tl;
   return true;
@@ -861,7 +861,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     if (!rowtile_tiling(plan.pmax, &tl)) return fail(SB_ERR_INVALID_ARGUMENT, "row-tile tiling");
     tl.nstrips = (g.W + sb::WS - 1) / sb::WS;
     const void* fn = sb::sweep_ptr_rowtile(k);
-    const size_t smem = (size_t)tl.obuf_off + 128 + (size_t)4 * sb::TOG * 2 * sb::TB * 32 * sizeof(float);
+    const size_t smem = (size_t)tl.obuf_off + 128 + (size_t)4 * sb::TOG * sb::TOBUF * sb::TB * 32 * sizeof(float);
     FnFacts ff;
     DevFacts df;
     rc = launch_facts(fn, smem, &ff, &df);

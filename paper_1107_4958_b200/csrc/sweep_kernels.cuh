@@ -1455,7 +1455,10 @@ constexpr int FRING = 32;  // max ring slots (512 TMEM columns / HB)
 //    tl.ds bands (copy_e = lag - span lets the loader run lag - span - CG + 1
 //    bands of slack ahead of the output groups).  The host classifies every trail window as ring or copy
 //    (tl.deepmask) and falls back to cols_kernel when a window would straddle.
-constexpr int CG = 3;                          // output warp groups
+#ifndef SB_CG
+#define SB_CG 3
+#endif
+constexpr int CG = SB_CG;                      // output warp groups
 constexpr int C2THREADS = 32 * 4 * (1 + CG);   // loader group + CG output groups
 constexpr int C2DONE = 32;  // output-band done barriers: >= lag - span + 1, so no barrier is lapped
 constexpr int C2PF = 8;     // max plane-band slots (TMA ring)
@@ -1533,6 +1536,10 @@ constexpr int TOG = SB_TOG;
 constexpr int TROWW = SB_TROWW;
 constexpr int TTHREADS = 32 * (TROWW + 4 + 4 * TOG);
 constexpr int TRS = SB_TRS;
+#ifndef SB_TOBUF
+#define SB_TOBUF 2
+#endif
+constexpr int TOBUF = SB_TOBUF;  // output boxes per output warp (double or single buffered)
 constexpr int TRSW = WS + 4;
 constexpr int TDONE = 32;  // output-band done barriers
 

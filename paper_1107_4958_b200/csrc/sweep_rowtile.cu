@@ -83,6 +83,10 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int
   sb_perturb();
 }
 
+#ifndef SB_RT_OUT_BACKOFF
+#define SB_RT_OUT_BACKOFF 1
+#endif
+
 // Position in the CTA's band list: band pb of segment w, CTA-global index gb.
 struct BandCursor {
   WorkIter w;
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(TTHREADS, 1)
         const int j0 = ob * TB;
         const int nb = min(TB, so.b - so.a - j0);
         const uint32_t need = so.gb0 + (uint32_t)((j0 + nb + 2 * t.pmax) / TB);
-        wait_above(&ring_cnt[q], need, true);
+        wait_above(&ring_cnt[q], need, SB_RT_OUT_BACKOFF);
         tmem_fence_after();
         const int out_mod = (int)(((so.gb0 + (uint32_t)ob) % (uint32_t)NBR) * TB);
         float2 o2[TB / 2];
@@ -338,8 +342,13 @@ __global__ void __launch_bounds__(TTHREADS, 1)
         if (lane == 0) st_release(&out_cnt[grp][q], onum / TOG + 1);
         const int out_row = so.a + j0 - g.oy0;
         if (g.out_bulk && nb == TB) {
-          float* obp = obuf + (ow * 2 + obsel) * (TB * 32);
-          if (lane == 0) bulk_wait_read<1>();  // the stores out of this box (two bands ago) have read it
+          float* obp = obuf + (ow * TOBUF + (TOBUF == 2 ? obsel : 0)) * (TB * 32);
+          if (lane == 0) {  // the stores out of this box (TOBUF bands ago) have read it
+            if (TOBUF == 2)
+              bulk_wait_read<1>();
+            else
+              bulk_wait_read<0>();
+          }
           __syncwarp();
 #pragma unroll
           for (int r = 0; r < TB / 2; ++r) {

@@ -149,3 +149,28 @@ def test_every_valid_kernel_has_a_path(lib):
     r, wt, rp, wp = _k(big.radii, big.weights)
     assert lib.sb_filter_rows_workspace_bytes(nat.SB_DTYPE_F32, 4, 100000, rp, 3) > 0
     assert lib.sb_filter_rows_workspace_bytes(nat.SB_DTYPE_F32, 4, 8000, rp, 3) == 0
+
+
+def test_one_launch_routing_per_policy(lib):
+    """Host routing of the one-launch kernels (no GPU needed: the workspace query runs the
+    same route as the launch).  AUTO: float32 one launch up to p_max 31 (fused_kernel), two
+    launches past it; SB_PATH_FUSED_WIDE extends the one-launch range to every float32 radius
+    the wide sweep's tiling admits (p_max <= 279 for k = 1, C5's 257 included) and leaves interleaved channels and
+    float64 on the two-launch path; SB_PATH_U8_ROWTILE keeps uint8 at one launch."""
+
+    def ws(dtype, p, ch=1):
+        r = (ctypes.c_int64 * 1)(p)
+        return lib.sb_separable_filter_2d_workspace_bytes(dtype, 1, 4096, 4096, ch, r, 1)
+
+    assert ws(nat.SB_DTYPE_F32, 31) == 0 and ws(nat.SB_DTYPE_F32, 32) > 0 and ws(nat.SB_DTYPE_F32, 257) > 0
+    with nat.path_policy(nat.SB_PATH_FUSED_WIDE):
+        for p in (32, 82, 170, 257, 279):
+            assert ws(nat.SB_DTYPE_F32, p) == 0, p
+        assert ws(nat.SB_DTYPE_F32, 280) > 0            # past its shared-memory budget: two launches
+        assert ws(nat.SB_DTYPE_F32, 170, ch=3) > 0      # interleaved channels: two launches
+        assert ws(nat.SB_DTYPE_F64, 100) > 0
+    assert ws(nat.SB_DTYPE_F32, 82) > 0                 # the policy is scoped
+    with nat.path_policy(nat.SB_PATH_U8_ROWTILE):
+        for p in (0, 7, 23, 100):
+            assert ws(nat.SB_DTYPE_U8, p) == 0, p
+    assert lib.sb_set_path_policy(nat.SB_PATH_U8_ROWTILE + 1) == -1
