@@ -31,58 +31,6 @@
 
 namespace sb {
 
-// Monotonic counters in shared memory (release / acquire at CTA scope): a count cannot alias
-// the way an mbarrier phase parity can when one waiter falls two phases behind.
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  sb_perturb();
-  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// SB_WATCHDOG builds: a wait longer than 2 s prints what it waited for and traps (a hang
-// becomes a diagnosable launch error)
-#ifdef SB_WATCHDOG
-#define SB_WD_START const unsigned long long wd_t0 = gtimer();
-#define SB_WD_CHECK(what, a, b)                                                                              \
-  if (gtimer() - wd_t0 > 2000000000ull) {                                                                    \
-    printf("watchdog: %s block %d warp %d lane %d a=%d b=%d\n", what, (int)blockIdx.x, (int)(threadIdx.x >> 5), \
-           (int)(threadIdx.x & 31), (int)(a), (int)(b));                                                     \
-    __trap();                                                                                                \
-  }
-#else
-#define SB_WD_START
-#define SB_WD_CHECK(what, a, b)
-#endif
-
-// wait until *p > v
-__device__ __forceinline__ void wait_above(const uint32_t* p, uint32_t v, bool backoff) {
-  unsigned ns = 32;
-  SB_WD_START
-  while (ld_acquire(p) <= v) {
-    SB_WD_CHECK("wait_above", v, ld_acquire(p));
-    if (backoff) {
-      __nanosleep(ns);
-      ns = ns < 256 ? 2 * ns : ns;
-    }
-  }
-  sb_perturb();
-}
-__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int tag) {
-  SB_WD_START
-  while (!mbar_test(bar, parity)) {
-    SB_WD_CHECK("mbar", tag, parity);
-  }
-  sb_perturb();
-}
-
 #ifndef SB_RT_OUT_BACKOFF
 #define SB_RT_OUT_BACKOFF 1
 #endif
