@@ -1601,7 +1601,8 @@ __global__ void __launch_bounds__(C2THREADS, 1)
                  const __grid_constant__ CUtensorMap omap, const __grid_constant__ CUtensorMap mmap) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
-  __shared__ __align__(8) uint64_t full[FRING], done[C2DONE], lfull[C2PF], lempty[C2PF];
+  __shared__ __align__(8) uint64_t done[C2DONE], lfull[C2PF], lempty[C2PF];
+  __shared__ uint32_t ring_cnt[4];  // ring bands written, per lane quadrant (monotonic: cannot alias)
   const int ch = blockIdx.x % g.in_px;
   const int sidx = blockIdx.x / g.in_px;
   const int strip = sidx % tl.nstrips;
@@ -1621,7 +1622,7 @@ __global__ void __launch_bounds__(C2THREADS, 1)
   int* dring = lring + PF * 2 * HB * WS;      // [DS + 1][HB][WS] copies of old ring bands (+ mirror of slot 0)
   float* obuf = (float*)(abase + tl.obuf_off);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NB; ++i) mbar_init(&full[i], 32 * 4);
+    for (int i = 0; i < 4; ++i) ring_cnt[i] = 0;
     for (int i = 0; i < C2DONE; ++i) mbar_init(&done[i], 32 * 4);
     for (int i = 0; i < PF; ++i) {
       mbar_init(&lfull[i], 1);   // the issuing thread's expect_tx + the TMA bytes
@@ -1726,8 +1727,9 @@ __global__ void __launch_bounds__(C2THREADS, 1)
         }
         tmem_wait_st();
         tmem_fence_before();
-        mbar_arrive(&full[slot0]);
-        if (nbp == 2) mbar_arrive(&full[slot0 + 1 == NB ? 0 : slot0 + 1]);
+        __syncwarp();
+        if (lane == 0) st_release(&ring_cnt[q], v + (uint32_t)nbp);  // this quadrant's bands < v + nbp
+        (void)slot0;
         if (DS > 0) {
           // after releasing band v: copy band u = v - NB + copy_e out of the ring (its
           // readers wait for band v + 1 or later; see cols_prefix_tiling)
@@ -1766,9 +1768,6 @@ __global__ void __launch_bounds__(C2THREADS, 1)
     // ------------------------------------------------ output groups
     const int grp = warp / 4 - 1;
     const int ow = warp - 4;  // output warp 0 .. 4*CG-1 (staging buffers)
-    uint32_t ready = 0;       // ring bands observed full
-    int rslot = 0;
-    uint32_t rph = 0;
     uint32_t onum = 0;
     int obsel = 0;
     SegIter so;
@@ -1781,24 +1780,11 @@ __global__ void __launch_bounds__(C2THREADS, 1)
         const int nb = min(HB, so.b - out_next);
         const uint32_t j = so.gb0 + (uint32_t)ob;  // ring band of the band's deepest trail row
         const uint32_t need = so.gb0 + (uint32_t)((ob * HB + nb + 2 * t.pmax) / HB);
-        // in order (a group's first band may need a band more than a ring ahead, so phases are
-        // observed one by one).  Without band copies (ring only, e.g. C4) the groups back off so
-        // their polling leaves issue slots to the loader (C4 1.231 -> 1.184 ms); with copies (C5)
-        // the ring is tight and the loader waits on the groups, so they spin (4.49 vs 4.54 ms).
-        const bool backoff = DS == 0;
-        while (ready <= need) {
-          if (backoff) {
-            for (unsigned ns = 32; !mbar_test(&full[rslot], rph); ns = ns < 256 ? 2 * ns : ns) __nanosleep(ns);
-            sb_perturb();
-          } else {
-            mbar_wait(&full[rslot], rph);
-          }
-          if (++rslot == NB) {
-            rslot = 0;
-            rph ^= 1;
-          }
-          ++ready;
-        }
+        // one monotonic count per lane quadrant (the loader fills the ring in order).  Without
+        // band copies (ring only, e.g. C4) the groups back off so their polling leaves issue
+        // slots to the loader (C4 1.231 -> 1.181 ms); with copies (C5) the ring is tight and
+        // the loader waits on the groups, so they spin.
+        wait_above(&ring_cnt[q], need, DS == 0);
         tmem_fence_after();
         const int base = (int)(j % (uint32_t)NB) * HB;  // ring position of virtual row 16*ob
         float2 o2[HB / 2];

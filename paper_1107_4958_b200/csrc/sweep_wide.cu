@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(WTHREADS, 1)
                   const __grid_constant__ CUtensorMap omap) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
-  __shared__ __align__(8) uint64_t full[FRING], done[C2DONE], sfull[WPROD], pfull[WPROD];
+  __shared__ __align__(8) uint64_t done[C2DONE], sfull[WPROD], pfull[WPROD];
+  __shared__ uint32_t ring_cnt[4];  // ring bands written, per lane quadrant (monotonic: cannot alias)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3;  // TMEM lane quadrant: columns 32q .. 32q+31
   const int c = 32 * q + lane;
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(WTHREADS, 1)
   int* dring = slots + FP * HB * LSW;               // [DS + 1][HB][WS] copies of old ring bands (+ mirror)
   float* obuf = (float*)(abase + tl.obuf_off);      // [4 * WCG][2][HB][32] output boxes (TMA stores)
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NB; ++i) mbar_init(&full[i], 32 * 4);
+    for (int i = 0; i < 4; ++i) ring_cnt[i] = 0;
     for (int i = 0; i < C2DONE; ++i) mbar_init(&done[i], 32 * 4);
     for (int i = 0; i < WPROD; ++i) {
       mbar_init(&sfull[i], 1);       // the issuing lane's expect_tx arrive + the bulk-copy bytes
@@ -268,8 +269,9 @@ __global__ void __launch_bounds__(WTHREADS, 1)
         }
         tmem_wait_st();
         tmem_fence_before();
-        mbar_arrive(&full[slot0]);
-        if (nbp == 2) mbar_arrive(&full[slot0 + 1 == NB ? 0 : slot0 + 1]);
+        __syncwarp();
+        if (lane == 0) st_release(&ring_cnt[q], v + (uint32_t)nbp);  // this quadrant's bands < v + nbp
+        (void)slot0;
         if (DS > 0) {
           // after releasing band v: copy band u = v - NB + copy_e out of the ring (its
           // readers wait for band v + 1 or later; see fusedw_tiling)
@@ -309,9 +311,6 @@ __global__ void __launch_bounds__(WTHREADS, 1)
     // ------------------------------------------------ output groups
     const int grp = warp / 4 - 1;
     const int ow = warp - 4;  // output warp 0 .. 4*WCG-1 (staging buffers)
-    uint32_t ready = 0;       // ring bands observed full
-    int rslot = 0;
-    uint32_t rph = 0;
     uint32_t onum = 0;
     int obsel = 0;
     WorkIter so;
@@ -325,17 +324,8 @@ __global__ void __launch_bounds__(WTHREADS, 1)
         const int nb = min(HB, so.b - out_next);
         const uint32_t j = so.gb0 + (uint32_t)ob;  // ring band of the band's deepest trail row
         const uint32_t need = so.gb0 + (uint32_t)((ob * HB + nb + 2 * t.pmax) / HB);
-        while (ready <= need) {
-          // the output groups mostly wait for the row warps: back off instead of spinning, so
-          // their polling does not take issue slots from the row and producer warps
-          for (unsigned ns = 64; !mbar_test(&full[rslot], rph); ns = ns < 512 ? 2 * ns : ns) __nanosleep(ns);
-          sb_perturb();
-          if (++rslot == NB) {
-            rslot = 0;
-            rph ^= 1;
-          }
-          ++ready;
-        }
+        // the output groups mostly wait for the row warps: back off instead of spinning
+        wait_above(&ring_cnt[q], need, true);
         tmem_fence_after();
         const int rbase = (int)(j % (uint32_t)NB) * HB;  // ring position of virtual row 16*ob
         float2 o2[HB / 2];
