@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(128) filter_at_rows_kernel(const Tin* __restri
     covered = t.p[i];
     acc = fmaf(t.w_row[i], __ll2float_rn(box), acc);
   }
-  R[(long long)ci * H + y] = __float_as_int(acc + kMagic) - kMagicBits;
+  R[(long long)ci * H + y] = __float_as_int(__fadd_rn(acc, kMagic)) - kMagicBits;  // _rn: never contracted into the last product
   report_status(status, bad, t);
 }
 

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(GT) rows_generic_kernel(const Tin* __restrict_
         acc = fmaf(TO_MID ? t.w_row[i] : t.w_out1[i], Acc<A>::to_f32(box_sum<U>(I, x, t.p[i], g.W, f0, fl)), acc);
       if constexpr (TO_MID) {
         mid_out[ch * g.mid_ch + (long long)img * g.mid_img + (long long)y * g.mid_row + x] =
-            (A)(__float_as_int(acc + kMagic) - kMagicBits);
+            (A)(__float_as_int(__fadd_rn(acc, kMagic)) - kMagicBits);  // _rn: never contracted (k = 1)
       } else {
         dst[(long long)img * g.out_img + (long long)y * g.out_row + (long long)x * g.out_px + ch] = acc;
       }

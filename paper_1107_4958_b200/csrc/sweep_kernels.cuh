@@ -307,6 +307,19 @@ __device__ __forceinline__ float i2f_fast(uint32_t x) {
   return f;
 }
 
+// Rounding of packed row values to the mid quantum (x + 1.5*2^23) as its own rounding step on
+// every path.  ptxas 12.9 contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 despite the explicit
+// rounding modifiers, so a one-slice kernel (a single FMUL2 before the add) would round once
+// where the scalar paths round twice: for K = 1 the add is done on the halves (add.rn.f32 is
+// honoured); for K >= 2 the preceding op is already an FFMA2 and nothing can be contracted.
+template <int K>
+__device__ __forceinline__ float2 round_mid2(float2 a) {
+  if constexpr (K == 1)
+    return make_float2(__fadd_rn(a.x, 12582912.0f), __fadd_rn(a.y, 12582912.0f));
+  else
+    return __fadd2_rn(a, make_float2(12582912.0f, 12582912.0f));
+}
+
 template <typename T>
 struct SrcTraits;
 template <>
@@ -794,7 +807,7 @@ __global__ void __launch_bounds__(WS) rows_kernel(const Tin* __restrict__ src, i
           if (r < n) {
             if constexpr (M == Mode::RowsToMid) {
               mid_out[ch * g.mid_ch + (long long)img * g.mid_img + (long long)(v0 + r) * g.mid_row + x0 + c] =
-                  __float_as_int(rv[r] + kMagic) - kMagicBits;
+                  __float_as_int(__fadd_rn(rv[r], kMagic)) - kMagicBits;
             } else {
               dst[(long long)img * g.out_img + (long long)(v0 + r) * g.out_row + (long long)(x0 + c) * g.out_px + ch] =
                   rv[r];
@@ -1188,7 +1201,7 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
             mbar_arrive(&bar_empty[pbi]);
 #pragma unroll
             for (int q = 0; q < HB / 2; ++q) {
-              r2[q] = __fadd2_rn(r2[q], make_float2(kMagic, kMagic));  // round to the mid quantum
+              r2[q] = round_mid2<K>(r2[q]);  // round to the mid quantum
               cv[h * HB + q] = __float_as_uint(r2[q].x);
               cv[h * HB + q + HB / 2] = __float_as_uint(r2[q].y);
             }
@@ -1294,14 +1307,14 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
           band_rows_f2<K>((const float2*)P, c, t, tl, r2);
 #pragma unroll
           for (int q = 0; q < HB / 2; ++q) {
-            r2[q] = __fadd2_rn(r2[q], make_float2(kMagic, kMagic));  // round to the mid quantum
+            r2[q] = round_mid2<K>(r2[q]);  // round to the mid quantum
             rv[q] = r2[q].x;
             rv[q + HB / 2] = r2[q].y;
           }
         } else {
           band_rows<K, PLS>(P, c, t.w_row, t, tl, rv);
 #pragma unroll
-          for (int r = 0; r < HB; ++r) rv[r] += kMagic;  // round to the mid quantum
+          for (int r = 0; r < HB; ++r) rv[r] = __fadd_rn(rv[r], kMagic);  // round to the mid quantum (_rn: never contracted)
         }
         mbar_arrive(&bar_empty[pbi]);
         {
@@ -2053,7 +2066,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
           if (x < g.W) {
 #pragma unroll
             for (int r = 0; r < HB / 2; ++r) {
-              const float2 q = __fadd2_rn(rv[h][r], make_float2(kMagic, kMagic));  // round to the mid quantum
+              const float2 q = round_mid2<K>(rv[h][r]);  // round to the mid quantum
               if (2 * r < nrows) midrow[2 * r][x] = __float_as_int(q.x) - kMagicBits;
               if (2 * r + 1 < nrows) midrow[2 * r + 1][x] = __float_as_int(q.y) - kMagicBits;
             }

@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(TTHREADS, 1)
         }
 #pragma unroll
         for (int j = 0; j < 8; j += 2) {
-          const float2 a = __fadd2_rn(acc[j], make_float2(kMagic, kMagic));  // round to the mid quantum
-          const float2 c = __fadd2_rn(acc[j + 1], make_float2(kMagic, kMagic));
+          const float2 a = round_mid2<K>(acc[j]);  // round to the mid quantum
+          const float2 c = round_mid2<K>(acc[j + 1]);
           *(float4*)(rrow + c0 + 2 * j) = make_float4(a.x, a.y, c.x, c.y);
         }
       }

@@ -250,8 +250,8 @@ __global__ void __launch_bounds__(WTHREADS, 1)
           int odd = cprefix;
 #pragma unroll
           for (int r = 0; r < HB; r += 2) {
-            const int e0 = __float_as_int(acc[r] + kMagic) - kMagicBits;
-            const int e1 = __float_as_int(acc[r + 1] + kMagic) - kMagicBits;
+            const int e0 = __float_as_int(__fadd_rn(acc[r], kMagic)) - kMagicBits;  // _rn: never contracted
+            const int e1 = __float_as_int(__fadd_rn(acc[r + 1], kMagic)) - kMagicBits;
             cv[d][r] = (uint32_t)(odd + e0);
             odd = odd + e0 + e1;
             cv[d][r + 1] = (uint32_t)odd;
