@@ -71,3 +71,47 @@ def test_every_policy_bit_identical(seed):
             ref = O.separable_filter_2d(np.ascontiguousarray(img), kern.radii, kern.weights)
             res = base[bi, :, :, c] if ch > 1 else base[bi]
             assert np.abs(res - ref).max() <= tol, (seed, h, w, dtype, ch, batch, kern)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SB_SWEEP_SEEDS", "24"))))
+def test_windows_rows_and_wide_radii_bit_identical(seed):
+    """The row-window entry point (strip partition), the row pass alone (filter_rows), very
+    large radii (2 p_max + 1 > 2048: int64 generic kernels) and rows that are not 16-byte
+    aligned (a column-sliced view), under every policy: the same bits as the default route."""
+    rng = np.random.default_rng(88000 + seed)
+    dtype = [np.float32, np.uint8, np.float64, np.uint16][seed % 4]
+    wide = seed % 6 == 0
+    h = int(rng.integers(2200, 2600)) if wide else int(rng.integers(3, 600))
+    w = int(rng.integers(2200, 2600)) if wide and seed % 12 == 0 else int(rng.integers(3, 600))
+    reach = min(h, w) - 1
+    k = int(min(rng.integers(1, 9), reach + 1))
+    top = reach if wide else min(reach, [40, 260, 120][seed % 3])
+    lo = min(1030, top) if wide else 0
+    pool = np.arange(lo, top + 1)
+    if pool.size < k:
+        pool = np.arange(0, reach + 1)
+    radii = np.sort(rng.choice(pool, size=k, replace=False))
+    kern = A.SliceKernel(radii, rng.uniform(0.1, 1.0, size=k)).normalized()
+    scale = {np.uint8: 255, np.uint16: 65535, np.float32: 255.0, np.float64: 1000.0}[dtype]
+    bound = None if dtype in (np.uint8, np.uint16) else float(scale)
+    full = torch.from_numpy((rng.random((h, w + 1)) * scale).astype(dtype)).cuda()
+    x = full[:, 1:] if seed % 2 else full[:, :w]  # odd seeds: rows 1 element off alignment
+    r0 = int(rng.integers(0, h))
+    r1 = int(rng.integers(r0 + 1, h + 1))
+
+    def run(policy):
+        with nat.path_policy(policy):
+            a = F.separable_filter_window(x, kern, r0, r1, value_bound=bound).cpu().numpy()
+            b = F.filter_rows(x, kern, value_bound=bound).cpu().numpy()
+        return a, b
+
+    base_w, base_r = run(nat.SB_PATH_AUTO)
+    for pol in (nat.SB_PATH_GENERIC, nat.SB_PATH_UNFUSED, nat.SB_PATH_FUSED_WIDE, nat.SB_PATH_U8_ROWTILE):
+        got_w, got_r = run(pol)
+        np.testing.assert_array_equal(got_w, base_w, err_msg=f"window, policy {pol} seed {seed}")
+        np.testing.assert_array_equal(got_r, base_r, err_msg=f"rows, policy {pol} seed {seed}")
+    if not wide:  # the oracle on a band of the window (full columns at this size are cheap)
+        xn = np.ascontiguousarray(x.cpu().numpy(), np.float64)
+        ref = O.filter_band(xn, kern.radii, kern.weights, r0, r1, threads=8)
+        tol = BAR * float(scale) / 255.0
+        assert np.abs(base_w - ref).max() <= tol, (seed, h, w, dtype, kern)
