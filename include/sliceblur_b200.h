@@ -64,8 +64,11 @@ enum {
   SB_PATH_FUSED_WIDE = 5,   /* float32 one-channel, radii past the fused sweep: one launch, the row
                                values never in HBM (DRAM 1.05x algorithmic; slower than the default
                                two-launch path at these radii); else as AUTO          */
-  SB_PATH_U8_ROWTILE = 6    /* uint8 one-channel, small radii: the row-tile sweep (row pass on
+  SB_PATH_U8_ROWTILE = 6,   /* uint8 one-channel, small radii: the row-tile sweep (row pass on
                                thread-per-row warps with the row prefix in TMEM); else as AUTO      */
+  SB_PATH_U8_PAIRED = 7,    /* uint8 fused sweep: two consumer warps per TMEM lane quadrant that
+                               alternate bands (eight consumer warps per CTA); else as AUTO         */
+  SB_PATH_U8_TWO_BAND = 8   /* uint8 fused sweep: four consumer warps, two bands per turn           */
 };
 
 /* return codes */

@@ -37,6 +37,8 @@ SB_PATH_U8_THREE_CTA = 3
 SB_PATH_U8_ONE_BAND = 4
 SB_PATH_FUSED_WIDE = 5
 SB_PATH_U8_ROWTILE = 6
+SB_PATH_U8_PAIRED = 7
+SB_PATH_U8_TWO_BAND = 8
 
 #: Every symbol include/sliceblur_b200.h declares (tests check the exports).
 EXPORTED_SYMBOLS = (

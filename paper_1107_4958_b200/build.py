@@ -40,17 +40,26 @@ def deps():
 STAMP = OUT + ".flags"
 
 
+def _stamp() -> str:
+    """Extra flags + a hash of the sources, taken when a build STARTS: a source edited while
+    nvcc was running must not look built, and a copied tree (new mtimes) must."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for p in deps():
+        with open(p, "rb") as f:
+            h.update(os.path.basename(p).encode() + b"\0" + f.read())
+    return os.environ.get("SB_NVCC_EXTRA", "") + "\n" + h.hexdigest()
+
+
 def up_to_date() -> bool:
     if not os.path.exists(OUT):
         return False
     try:
         with open(STAMP) as f:
-            if f.read() != os.environ.get("SB_NVCC_EXTRA", ""):
-                return False  # built with other extra flags
+            return f.read() == _stamp()
     except OSError:
         return False
-    built = os.path.getmtime(OUT)
-    return all(os.path.getmtime(p) <= built for p in deps())
 
 
 def nvcc() -> str:
@@ -66,6 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     from concurrent.futures import ThreadPoolExecutor
 
+    stamp = _stamp()
     objdir = os.path.join(PKG, "build_obj")
     os.makedirs(objdir, exist_ok=True)
     flags = [f for f in NVCC_FLAGS if f != "-shared"] + os.environ.get("SB_NVCC_EXTRA", "").split()
@@ -85,7 +95,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs], check=True)
     os.replace(tmp, OUT)
     with open(STAMP, "w") as f:
-        f.write(os.environ.get("SB_NVCC_EXTRA", ""))
+        f.write(stamp)
     return OUT
 
 

@@ -41,6 +41,10 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 constexpr size_t kSmemBudget = 200 * 1024;
+// the automatic uint8 one-channel kernel: paired consumer warps (1) or two bands per turn (0)
+#ifndef SB_U8_DEFAULT_PAIRED
+#define SB_U8_DEFAULT_PAIRED 0
+#endif
 
 int ceil16(int v) { return (v + 15) & ~15; }
 
@@ -228,7 +232,21 @@ sb::Tiling make_tiling(sb::Mode m, int pmax, int channels, int es, bool u8_singl
     // SB_FUSED=3: fused_kernel<uint8_t, K, 3>, three CTAs per SM (registers rebalanced between
     // the producer and consumer warpgroups with setmaxnreg, single-buffered staging and output
     // box).  SB_FUSED=1: the two-CTA one-band kernel.  (A/B switches.)
-    if (g_policy != SB_PATH_U8_THREE_CTA && g_policy != SB_PATH_U8_ONE_BAND) {
+    // SB_U8_DEFAULT_PAIRED picks the automatic uint8 kernel: paired consumer warps (1) or two
+    // bands per consumer turn (0); SB_PATH_U8_PAIRED / SB_PATH_U8_TWO_BAND force either
+    const bool paired = g_policy == SB_PATH_U8_PAIRED || (SB_U8_DEFAULT_PAIRED && g_policy != SB_PATH_U8_TWO_BAND &&
+                                                          g_policy != SB_PATH_U8_THREE_CTA &&
+                                                          g_policy != SB_PATH_U8_ONE_BAND);
+    if (paired) {
+      // ring: the bands one output band reads (E + 1) plus three bands of slack, so a band is
+      // overwritten only after the other warp has left every window that reads it
+      tl.split = 6;
+      const int E = (2 * pmax + 1 + 2 * sb::HB - 1) / sb::HB - 1;
+      tl.D = (E + 4) * sb::HB;
+      int colsp = 32;
+      while (colsp < tl.D + sb::HB) colsp <<= 1;
+      tl.tmem_cols = colsp;
+    } else if (g_policy != SB_PATH_U8_THREE_CTA && g_policy != SB_PATH_U8_ONE_BAND) {
       // two bands per consumer iteration: 32-row ring slots, 32-row mirror
       tl.split = 5;
       tl.D = ((2 * pmax + 65 + 31) / 32) * 32;
@@ -258,7 +276,7 @@ size_t smem_bytes(const sb::Tiling& tl, sb::Mode m) {
     // staged bands + prefix buffers (producer/consumer hand-off); the ring lives in tensor memory.
     // + FCONS x 2 output bands of HB x 32 floats staged for TMA tensor stores
     // output staging per consumer warp: 1 (three-CTA), 2 (two-CTA) 16-row boxes, or two 32-row boxes (split 5)
-    const int boxes = tl.split == 3 ? 1 : (tl.split == 5 ? 4 : tl.nsb);
+    const int boxes = tl.split == 3 ? 1 : (tl.split == 5 || tl.split == 6 ? 4 : tl.nsb);
     size_t s = (size_t)tl.obuf_off + 128 + (size_t)sb::FCONS * boxes * sb::HB * 32 * sizeof(float);
     // cap residency at 512 / tmem_cols CTAs per SM by asking for enough shared
     // memory, so no CTA ever waits inside tcgen05.alloc
@@ -289,6 +307,19 @@ const void* pick_kernel(sb::Mode m, int dtype, int k) {
 // Tiling of the prefix-form column kernel (cols2_kernel): a 496-row TMEM ring,
 // CG output groups, trail windows classified as ring or band copies.  False when
 // a window would straddle the two (the running-sum cols_kernel is used then).
+// cols2_kernel runs one CTA per SM: its TMA slots and band copies may take the whole opt-in
+// shared memory (static shared memory is < 1 KB)
+#ifndef SB_COLS2_SMEM_KB
+#define SB_COLS2_SMEM_KB 224
+#endif
+constexpr size_t kCols2Smem = (size_t)SB_COLS2_SMEM_KB * 1024;
+#ifndef SB_COLS2_MINPF
+#define SB_COLS2_MINPF 2
+#endif
+#ifndef SB_COLS2_SLACK0
+#define SB_COLS2_SLACK0 3
+#endif
+
 bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int pmax, sb::Tiling* out) {
   sb::Tiling tl = base;
   const int NB = 31;
@@ -299,9 +330,13 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
   const int span = 2 + pmax / 8;  // ring bands one output band reads
   // Slack: bands the loader may run ahead of the output groups.  Without band copies the
   // ring bounds it (lag <= NB); with copies, each slack band costs two copy slots.
-  int slack = NB - span - sb::CG + 1;
-  if (slack < 0) slack = 3;
-  for (; slack >= 0; --slack) {
+  int slack0 = NB - span - sb::CG + 1;
+  if (slack0 < 0) slack0 = SB_COLS2_SLACK0;
+  // first pass: the most slack that still leaves SB_COLS2_MINPF TMA slots (bytes in flight per
+  // SM); second pass: anything that fits
+  for (int it = 0; it < 2 * (slack0 + 1); ++it) {
+    const int slack = slack0 - (it % (slack0 + 1));
+    const int min_pf = it <= slack0 ? SB_COLS2_MINPF : 2;
     tl.lag = span + sb::CG - 1 + slack;
     tl.copy_e = tl.lag - span + 1;  // band v - NB + copy_e is copied right after band v is released
     // output band o + C2DONE may finish before the loader observed band o's done phase
@@ -322,11 +357,11 @@ bool cols_prefix_tiling(const sb::Tiling& base, const int64_t* radii, int k, int
     tl.pf = 0;
     const int copies = tl.ds ? tl.ds + 1 : 0;  // + the mirror of copy slot 0
     for (int pf : {sb::C2PF, 6, 4, 3, 2})      // slots of two bands each
-      if ((size_t)(2 * pf + copies) * band + obuf <= kSmemBudget) {
+      if ((size_t)(2 * pf + copies) * band + obuf <= kCols2Smem) {
         tl.pf = pf;
         break;
       }
-    if (!tl.pf) continue;
+    if (tl.pf < min_pf) continue;
     tl.obuf_off = (int)((size_t)(2 * tl.pf + copies) * band);
     *out = tl;
     return true;
@@ -514,7 +549,8 @@ int plan_launch(const void* fn, sb::Mode m, const sb::Tiling& base, int pmax, in
   const int sms = df.sms, smem_per_sm = df.smem_per_sm, regs_per_sm = df.regs_per_sm;
   // Residency from the kernel's own resources.  (cudaOccupancyMaxActiveBlocksPerMultiprocessor
   // reports 1 for kernels that allocate tensor memory, which would idle 3/4 of each SM.)
-  const int threads = (m == sb::Mode::Fused) ? sb::FTHREADS : (m == sb::Mode::ColsPrefix ? sb::C2THREADS : sb::WS);
+  const int threads = (m == sb::Mode::Fused) ? (tl.split == 6 ? sb::PTHREADS : sb::FTHREADS)
+                                             : (m == sb::Mode::ColsPrefix ? sb::C2THREADS : sb::WS);
   const int regs_per_cta = ((fa.num_regs * 32 + 255) / 256) * 256 * (threads / 32);
   occ = std::min(2048 / threads, regs_per_sm / std::max(1, regs_per_cta));
   occ = std::min<long long>(occ, (long long)smem_per_sm / (long long)(smem + fa.static_smem + 1024));
@@ -629,7 +665,7 @@ int launch_fused(const void* fn, const Launch& L, const void* src, float* dst, c
   alignas(64) CUtensorMap omap;
   make_output_map(dst, g, &omap);
   void* args[] = {(void*)&src, (void*)&dst, (void*)&g, (void*)&t, (void*)&L.tl, (void*)&status, (void*)&omap};
-  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(sb::FTHREADS), args, L.smem, stream);
+  cudaError_t e = cudaLaunchKernel(fn, L.grid, dim3(L.tl.split == 6 ? sb::PTHREADS : sb::FTHREADS), args, L.smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   return SB_OK;
 }
@@ -735,7 +771,7 @@ extern "C" {
 int sb_version(void) { return 4; }
 
 int sb_set_path_policy(int policy) {
-  if (policy < SB_PATH_AUTO || policy > SB_PATH_U8_ROWTILE) return -1;
+  if (policy < SB_PATH_AUTO || policy > SB_PATH_U8_TWO_BAND) return -1;
   const int prev = g_policy;
   g_policy = policy;
   return prev;
@@ -849,6 +885,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     const sb::Tiling base = make_tiling(sb::Mode::Fused, plan.pmax, channels, g.es, u8_single);
     const void* fn = base.split == 3   ? sb::sweep_ptr_fused3(k)
                      : base.split == 5 ? sb::sweep_ptr_fused5(k)
+                     : base.split == 6 ? sb::sweep_ptr_fusedp(k)
                      : (src_dtype == SB_DTYPE_F32 && channels == 1) ? sb::sweep_ptr_fused_f32(k, base.ls)
                                                                      : pick_kernel(sb::Mode::Fused, src_dtype, k);
     Launch L;
@@ -935,7 +972,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     // streaming row pass: full-width bands, prefix carried across chunks
     const int xs = -(((plan.pmax + 1) + 15) & ~15);  // first halo column, 16-aligned
     const void* fs = sb::sweep_ptr_stream_f32(k);
-    const size_t smem = (size_t)sb::NPROD * 2 * 8 * (sb::CW * sizeof(float) + sb::SRB_PAD) +
+    const size_t smem = (size_t)sb::NPROD * sb::STG * 8 * (sb::CW * sizeof(float) + sb::SRB_PAD) +
                         (size_t)sb::HB * sb::RLS * sizeof(int);
     FnFacts ff;
     DevFacts df;
@@ -948,7 +985,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     if (debug_plans())
       std::fprintf(stderr, "[sliceblur_b200] stream rows: pmax=%d xs=%d bands=%d grid=%d x %d smem=%zu\n",
                    plan.pmax, xs, nb_total, gx, channels, smem);
-    cudaError_t e = cudaLaunchKernel(fs, dim3(gx * channels, 1), dim3(sb::FUSED_THREADS), args, smem, st);
+    cudaError_t e = cudaLaunchKernel(fs, dim3(gx * channels, 1), dim3(sb::STREAM_THREADS), args, smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   } else if (route.rows == RowPath::Tiled) {
     const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);

@@ -183,6 +183,12 @@ __device__ __forceinline__ void st_stream(float* p, float v) {
   asm volatile("st.global.cs.f32 [%0], %1;\n" ::"l"(p), "f"(v));
 }
 // ---- TMA tensor stores from shared memory (async proxy)
+// 32-bit word store at (global address base) + 4 * idx: one IMAD.WIDE per address
+__device__ __forceinline__ void st_global_idx(size_t base, int idx, int v) {
+  asm volatile("{\n\t.reg .u64 a;\n\tmad.wide.s32 a, %1, 4, %0;\n\tst.global.b32 [a], %2;\n\t}" ::"l"(base), "r"(idx),
+               "r"(v)
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* ssrc, int x, int y, int z) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
@@ -1052,20 +1058,88 @@ constexpr int FPBUF = 2 * FPROD;
 #endif
 constexpr int F3PREG = SB_F3PREG, F3CREG = SB_F3CREG;
 
-template <typename Tin, int K, int MINB = 2, bool B2 = false, int PLS = LS>
-__global__ void __launch_bounds__(FTHREADS, MINB)
+// ---- shared-memory counters (acquire / release) and the device watchdog used by the ring kernels
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  sb_perturb();
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// SB_WATCHDOG builds: a wait longer than 2 s prints what it waited for and traps (a hang
+// becomes a diagnosable launch error)
+#ifdef SB_WATCHDOG
+#define SB_WD_START const unsigned long long wd_t0 = gtimer();
+#define SB_WD_CHECK(what, a, b)                                                                              \
+  if (gtimer() - wd_t0 > 2000000000ull) {                                                                    \
+    printf("watchdog: %s block %d warp %d lane %d a=%d b=%d\n", what, (int)blockIdx.x, (int)(threadIdx.x >> 5), \
+           (int)(threadIdx.x & 31), (int)(a), (int)(b));                                                     \
+    __trap();                                                                                                \
+  }
+#else
+#define SB_WD_START
+#define SB_WD_CHECK(what, a, b)
+#endif
+
+// wait until *p > v
+__device__ __forceinline__ void wait_above(const uint32_t* p, uint32_t v, bool backoff) {
+  unsigned ns = 32;
+  SB_WD_START
+  while (ld_acquire(p) <= v) {
+    SB_WD_CHECK("wait_above", v, ld_acquire(p));
+    if (backoff) {
+      __nanosleep(ns);
+      ns = ns < 256 ? 2 * ns : ns;
+    }
+  }
+  sb_perturb();
+}
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int tag) {
+  SB_WD_START
+  while (!mbar_test(bar, parity)) {
+    SB_WD_CHECK("mbar", tag, parity);
+  }
+  sb_perturb();
+}
+
+// PAIRED (uint8 packed path): eight consumer warps.  Warps q and q + 4 share TMEM lane quadrant
+// q and alternate bands: each forms the row values of its own band while the other is still
+// in its column pass, takes the column prefix at the end of the previous band from the other
+// warp (one shared-memory word per column, monotonic per-quadrant counters), appends its band
+// to the ring and forms the output band that its band completes.  Twice the consumer warps per
+// SM for the latency-bound row-value / window chains, at 80 registers per thread.
+#ifndef SB_FPPREG
+#define SB_FPPREG 64
+#define SB_FPCREG 88
+#endif
+constexpr int PTHREADS = FTHREADS + 32 * FCONS;
+
+template <typename Tin, int K, int MINB = 2, bool B2 = false, int PLS = LS, bool PAIRED = false>
+__global__ void __launch_bounds__(PAIRED ? PTHREADS : FTHREADS, MINB)
     fused_kernel(const Tin* __restrict__ src, float* __restrict__ dst, Geometry g, Taps t, Tiling tl, int* status,
                  const __grid_constant__ CUtensorMap omap) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
   __shared__ __align__(8) uint64_t bar_full[FPBUF], bar_empty[FPBUF];
+  // PAIRED hand-offs: bands whose end-of-band column prefix is published (per quadrant), bands
+  // each consumer warp has appended to the ring, and the published prefixes (per writer half)
+  __shared__ uint32_t pair_cnt[4], stored_cnt[2 * FCONS], seg_cnt[2 * FCONS];
+  __shared__ int carry_s[2][WS];
+  constexpr int NCW = PAIRED ? 2 * FCONS : FCONS;  // consumer warps
   const int strip = blockIdx.x % tl.nstrips;
   const long long item = blockIdx.x / tl.nstrips;
   const int ch = blockIdx.y;
   const int x0 = strip * WS;
   const int xb = x0 - tl.xoff;
   const int warp = threadIdx.x >> 5;
-  const bool producer = warp >= FCONS;
+  const bool producer = warp >= NCW;
   const int wh = g.oy1 - g.oy0;  // rows of each image this launch outputs
   const long long total = (long long)g.nimg * wh;
   const long long T0 = item * tl.rows_per_item;
@@ -1086,11 +1160,21 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
       mbar_init(&bar_full[i], 32);  // one producer warp fills a prefix buffer
       mbar_init(&bar_empty[i], 32 * FCONS);
     }
+    if constexpr (PAIRED) {
+      for (int i = 0; i < 4; ++i) pair_cnt[i] = 0;
+      for (int i = 0; i < 2 * FCONS; ++i) stored_cnt[i] = seg_cnt[i] = 0;
+    }
   }
   if (warp == 0) tmem_alloc(&tmem_base_s, (uint32_t)tl.tmem_cols);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
+  if constexpr (PAIRED) {
+    if (producer)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SB_FPPREG));
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(SB_FPCREG));
+  }
   if constexpr (MINB == 3) {
     if (producer)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(F3PREG));
@@ -1103,7 +1187,7 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
     // Producer warp pw owns the bands with global index gb = pw (mod FPROD): it stages
     // them into its private pair of buffers (prefetching its next band) and scans
     // them into prefix buffer pw, so the producers never synchronise with each other.
-    const int lane = threadIdx.x & 31, pw = warp - FCONS;
+    const int lane = threadIdx.x & 31, pw = warp - NCW;
     const bool edge = (xb < 0) || (xb + tl.L > g.W);
     const int st_lo = max(xb, 0) * g.in_px * g.es;
     const int st_hi = min(xb + tl.L, g.W) * g.in_px * g.es;
@@ -1168,6 +1252,130 @@ __global__ void __launch_bounds__(FTHREADS, MINB)
       }
       gb0 += (uint32_t)nbands;
     }
+  } else if constexpr (PAIRED) {
+    // ------------------------------------------------ paired consumer warps (see the template comment)
+    const int lane = threadIdx.x & 31, q = warp & 3, hf = warp >> 2;
+    const int c = 32 * q + lane;
+    const bool active = (x0 + c) < g.W;
+    const uint32_t tlane = tmem_base_s + ((uint32_t)(32 * q) << 16);
+    const int NBR = D / HB;  // ring bands
+    uint32_t gb0 = 0;        // global index of the segment's first band
+    uint32_t seg = 0;        // segments completed
+    int obsel = 0;
+    for (long long T = T0; T < T1; ++seg) {
+      const int img = (int)(T / wh);
+      const int a = g.oy0 + (int)(T - (long long)img * wh);
+      const int b = g.oy0 + (int)min((long long)wh, T1 - (long long)img * wh);
+      T = (long long)img * wh + (b - g.oy0);
+      const int count = (b - a) + 2 * t.pmax + 1;
+      const int nbands = (count + HB - 1) / HB;
+      const int nob = (b - a + HB - 1) / HB;  // output bands of the segment
+      int ob = 0, obslot = 0;                 // next output band to consider, ob % NBR
+      int slot = hf;                          // ring band of this warp's next band (pb % NBR; NBR >= 2)
+      bool first = true;
+      for (int pb = hf; pb < nbands; pb += 2) {
+        const uint32_t gb = gb0 + (uint32_t)pb;
+        const int n = min(HB, count - pb * HB);
+        const uint32_t kb = gb / FPROD;
+        const int pbi = (int)(gb % FPROD) * tl.npb + (int)(kb & (uint32_t)(tl.npb - 1));
+        const float2* P = (const float2*)(Pbase + pbi * pbuf_words);
+        uint32_t cv[HB];
+        {
+          // A parity wait is only meaningful once the buffer's previous use (band gb - 4) is
+          // over.  Inside a segment the carry chain guarantees it (this warp's previous band
+          // gb - 2 needed every earlier band); a warp entering a segment may have been idle for
+          // many one-band segments, so it first sees band gb - 2 published.
+          if (first && gb >= 2) wait_above(&pair_cnt[q], gb - 2, false);
+          mbar_wait(&bar_full[pbi], (kb >> (tl.npb - 1)) & 1);
+          float2 r2[HB / 2];
+          band_rows_f2<K>(P, c, t, tl, r2);
+          mbar_arrive(&bar_empty[pbi]);
+          int lp = 0;  // prefix within the band
+#pragma unroll
+          for (int qq = 0; qq < HB / 2; ++qq) r2[qq] = round_mid2<K>(r2[qq]);  // round to the mid quantum
+#pragma unroll
+          for (int r = 0; r < HB; ++r) {
+            const float v = r < HB / 2 ? r2[r].x : r2[r - HB / 2].y;
+            lp += __float_as_int(v) - kMagicBits;
+            cv[r] = (uint32_t)lp;
+          }
+        }
+        // column prefix at the end of band gb - 1 (published by the other warp; 0 at a segment
+        // start).  Waiting also keeps pair_cnt monotonic: band gb is published after gb - 1.
+        if (gb > 0) wait_above(&pair_cnt[q], gb - 1, false);
+        const int carry = pb > 0 ? carry_s[hf ^ 1][c] : 0;
+#pragma unroll
+        for (int r = 0; r < HB; ++r) cv[r] += (uint32_t)carry;
+        carry_s[hf][c] = (int)cv[HB - 1];
+        __syncwarp();
+        if (lane == 0) st_release(&pair_cnt[q], gb + 1);
+        // the ring restarts with every segment: the other warp must be out of the previous
+        // segment's windows before this warp's first band lands
+        if (first && seg > 0) wait_above(&seg_cnt[2 * q + (hf ^ 1)], seg - 1, false);
+        first = false;
+        SB_ASSERT(slot * HB + HB <= D && D + HB <= tl.tmem_cols);
+        tmem_st16(tlane + (uint32_t)(slot * HB), cv);
+        if (slot == 0) tmem_st16(tlane + (uint32_t)D, cv);  // mirror: lag windows never wrap
+        tmem_wait_st();
+        tmem_fence_before();
+        __syncwarp();
+        if (lane == 0) st_release(&stored_cnt[2 * q + hf], gb + 1);
+        slot += 2;
+        slot = slot >= NBR ? slot - NBR : slot;
+        // output bands completed by this band (band ob needs virtual rows up to 16 ob + nb + 2 pmax)
+        while (ob < nob) {
+          const int nb = min(HB, (b - a) - ob * HB);
+          const int pe = (ob * HB + nb + 2 * t.pmax + 1 + HB - 1) / HB - 1;
+          if (pe > pb) break;
+          if (pe == pb) {
+            // every earlier band is in the ring: this warp's in program order, the other's by count
+            if (pb > 0) wait_above(&stored_cnt[2 * q + (hf ^ 1)], gb - 1, false);
+            tmem_fence_after();
+            const int out_next = a + ob * HB;
+            const int out_mod = obslot * HB;
+            int lead_s[K], trail_s[K];
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+              const int l = out_mod + t.pmax + 1 + t.p[i];
+              const int tr = out_mod + t.pmax - t.p[i];
+              lead_s[i] = l >= D ? l - D : l;
+              trail_s[i] = tr >= D ? tr - D : tr;
+            }
+            float ov[HB];
+            column_band_tmem<K>(tlane, lead_s, trail_s, t, ov);
+            if (g.out_bulk && nb == HB) {
+              float* obp = obuf + (warp * 2 + obsel) * (HB * 32);
+              if (lane == 0) bulk_wait_read<1>();  // the store out of this box (two bands ago) has read it
+              __syncwarp();
+#pragma unroll
+              for (int r = 0; r < HB; ++r) obp[r * 32 + lane] = ov[r];
+              fence_proxy_async();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(&omap, obp, x0 + 32 * q, out_next - g.oy0, img);
+                bulk_commit();
+              }
+              obsel ^= 1;
+            } else if (active) {
+              float* dptr = dst + (long long)img * g.out_img + (long long)(out_next - g.oy0) * g.out_row + (x0 + c);
+#pragma unroll
+              for (int r = 0; r < HB; ++r) {
+                if (r < nb) st_stream(dptr, ov[r]);
+                dptr += g.out_row;
+              }
+            }
+          }
+          ++ob;
+          obslot = obslot + 1 == NBR ? 0 : obslot + 1;
+        }
+      }
+      gb0 += (uint32_t)nbands;
+      // this warp has read its last window of the segment (tcgen05.wait::ld precedes the release)
+      tmem_fence_before();
+      __syncwarp();
+      if (lane == 0) st_release(&seg_cnt[2 * q + hf], seg + 1);
+    }
+    if (lane == 0) bulk_wait_read<0>();
   } else if constexpr (B2) {
     // ------------------------------------------------ consumer warps, two bands per iteration
     // (uint8 packed path): one prefix carry, one 32-column TMEM store, one 32-row output band
@@ -1425,7 +1633,8 @@ struct SegIter {
     load();
   }
 };
-inline const void* fused5_ptr_for(int k) {
+template <typename Unused = void>  // a template: instantiates its kernels only where it is called
+const void* fused5_ptr_for(int k) {
   switch (k) {
     case 1: return (const void*)fused_kernel<uint8_t, 1, 2, true>;
     case 2: return (const void*)fused_kernel<uint8_t, 2, 2, true>;
@@ -1438,7 +1647,22 @@ inline const void* fused5_ptr_for(int k) {
   }
 }
 
-inline const void* fused3_ptr_for(int k) {
+template <typename Unused = void>  // a template: instantiates its kernels only where it is called
+const void* fusedp_ptr_for(int k) {
+  switch (k) {
+    case 1: return (const void*)fused_kernel<uint8_t, 1, 2, false, LS, true>;
+    case 2: return (const void*)fused_kernel<uint8_t, 2, 2, false, LS, true>;
+    case 3: return (const void*)fused_kernel<uint8_t, 3, 2, false, LS, true>;
+    case 4: return (const void*)fused_kernel<uint8_t, 4, 2, false, LS, true>;
+    case 5: return (const void*)fused_kernel<uint8_t, 5, 2, false, LS, true>;
+    case 6: return (const void*)fused_kernel<uint8_t, 6, 2, false, LS, true>;
+    case 7: return (const void*)fused_kernel<uint8_t, 7, 2, false, LS, true>;
+    default: return (const void*)fused_kernel<uint8_t, 8, 2, false, LS, true>;
+  }
+}
+
+template <typename Unused = void>  // a template: instantiates its kernels only where it is called
+const void* fused3_ptr_for(int k) {
   switch (k) {
     case 1: return (const void*)fused_kernel<uint8_t, 1, 3>;
     case 2: return (const void*)fused_kernel<uint8_t, 2, 3>;
@@ -1534,55 +1758,6 @@ constexpr int WLS[3] = {516, 676, 900};
 
 // Monotonic counters in shared memory (release / acquire at CTA scope): a count cannot alias
 // the way an mbarrier phase parity can when one waiter falls two phases behind.
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  sb_perturb();
-  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// SB_WATCHDOG builds: a wait longer than 2 s prints what it waited for and traps (a hang
-// becomes a diagnosable launch error)
-#ifdef SB_WATCHDOG
-#define SB_WD_START const unsigned long long wd_t0 = gtimer();
-#define SB_WD_CHECK(what, a, b)                                                                              \
-  if (gtimer() - wd_t0 > 2000000000ull) {                                                                    \
-    printf("watchdog: %s block %d warp %d lane %d a=%d b=%d\n", what, (int)blockIdx.x, (int)(threadIdx.x >> 5), \
-           (int)(threadIdx.x & 31), (int)(a), (int)(b));                                                     \
-    __trap();                                                                                                \
-  }
-#else
-#define SB_WD_START
-#define SB_WD_CHECK(what, a, b)
-#endif
-
-// wait until *p > v
-__device__ __forceinline__ void wait_above(const uint32_t* p, uint32_t v, bool backoff) {
-  unsigned ns = 32;
-  SB_WD_START
-  while (ld_acquire(p) <= v) {
-    SB_WD_CHECK("wait_above", v, ld_acquire(p));
-    if (backoff) {
-      __nanosleep(ns);
-      ns = ns < 256 ? 2 * ns : ns;
-    }
-  }
-  sb_perturb();
-}
-__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int tag) {
-  SB_WD_START
-  while (!mbar_test(bar, parity)) {
-    SB_WD_CHECK("mbar", tag, parity);
-  }
-  sb_perturb();
-}
 
 // Row-tile sweep (sweep_rowtile.cu): uint8, one channel, small radii.  32-row bands; 8 row
 // warps (thread = row; two per TMEM lane quadrant), 4 loader warps and TOG output groups of 4
@@ -1905,15 +2080,31 @@ constexpr int RL = 1024;   // prefix ring length (power of two, >= 3*CW + 2*pmax
 constexpr int NSLOT = RL / CW;  // ring chunk slots; one full/done mbarrier per slot (no phase aliasing)
 constexpr int RLS = RL + 4;     // prefix ring row stride in words: 4112 B = 16 (mod 128)
 constexpr int SRB_PAD = 16;     // staged rows are CW*4 + 16 bytes apart: 16 (mod 128)
+// staged input chunks per producer warp: each warp keeps STG - 1 chunks (8 rows x CW) in flight
+// while it scans one, so the bytes in flight per SM cover the DRAM latency
+#ifndef SB_STREAM_STAGES
+#define SB_STREAM_STAGES 4
+#endif
+constexpr int STG = SB_STREAM_STAGES;
+// consumer warps: SRG row groups of CW threads; group rg forms rows [rg * HB / SRG, (rg + 1) * HB / SRG)
+// of each output chunk.  Two groups (8 rows per thread, 20 warps per SM instead of 12) measured
+// 3.7 % slower on C5 (4.416 vs 4.257 ms): the per-thread address work doubles.  Default 1.
+#ifndef SB_STREAM_ROWGROUPS
+#define SB_STREAM_ROWGROUPS 1
+#endif
+constexpr int SRG = SB_STREAM_ROWGROUPS;
+constexpr int SCONS = SRG * (CW / 32);
+constexpr int STREAM_THREADS = 32 * (SCONS + NPROD);
+constexpr int SHB = HB / SRG;  // rows per consumer thread
 
 template <typename Tin, int K>
-__global__ void __launch_bounds__(FUSED_THREADS, 2)
+__global__ void __launch_bounds__(STREAM_THREADS, 2)
     stream_rows_kernel(const Tin* __restrict__ src, int* __restrict__ mid_out, Geometry g, Taps t, int xs,
                        int nbands_total, int* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
   const int warp = threadIdx.x >> 5;
-  const bool producer = warp >= NCONS;
+  const bool producer = warp >= SCONS;
   const int qtotal = g.W - xs + t.pmax;  // virtual columns q = x - xs, x in [xs, W + pmax)
   const int nin = (qtotal + CW - 1) / CW;
   const int nout = (g.W + CW - 1) / CW;
@@ -1922,13 +2113,13 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
   // staged rows and prefix-ring rows are an odd multiple of 16 bytes apart, so the 8 lanes
   // of a 128-bit access phase (8 rows, same chunk) hit 8 distinct bank groups
   const int rowbytes = CW * (int)sizeof(Tin) + SRB_PAD;
-  unsigned char* stage = smem;                           // [NPROD][2][8][rowbytes]
-  int* P = (int*)(smem + NPROD * 2 * 8 * rowbytes);      // [HB][RLS]
+  unsigned char* stage = smem;                           // [NPROD][STG][8][rowbytes]
+  int* P = (int*)(smem + NPROD * STG * 8 * rowbytes);    // [HB][RLS]
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSLOT; ++i) {
       mbar_init(&bar_full[i], 32 * NPROD);
-      mbar_init(&bar_done[i], 32 * NCONS);
+      mbar_init(&bar_done[i], 32 * SCONS);
     }
   }
   __syncthreads();
@@ -1940,8 +2131,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
     const long long row0 = (long long)band * HB;
     const int nrows = (int)min((long long)HB, (long long)g.nimg * g.H - row0);
     if (producer) {
-      const int lane = threadIdx.x & 31, pw = warp - NCONS;
-      unsigned char* mystage = stage + pw * 2 * 8 * rowbytes;
+      const int lane = threadIdx.x & 31, pw = warp - SCONS;
+      unsigned char* mystage = stage + pw * STG * 8 * rowbytes;
       // this warp's 8 source rows (clamped at the end of the tall image) - hoisted per band
       const Tin* rowp[8];
 #pragma unroll
@@ -1981,18 +2172,31 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
       // lane -> row rr = lane & 7 of this warp's 8 and chunk (lane >> 3) + 4*pass of the 8
       // CH-column chunks; the row's running prefix (carry) lives in the 4 lanes of that row
       int carry = 0;
-      issue(0, 0);
+      // one commit group per chunk (empty past the end), so "at most STG - 2 groups pending"
+      // always means chunk j has landed
+#pragma unroll
+      for (int j = 0; j < STG - 1; ++j) {
+        if (j < nin)
+          issue(j, j);
+        else
+          cp_async_commit();
+      }
       RangeAcc bad;
+      int sbuf = 0;  // j % STG
       for (int j = 0; j < nin; ++j) {
         const uint32_t gj = cin_ctr + j;
-        cp_async_wait_all();
-        __syncwarp();
-        if (j + 1 < nin) issue(j + 1, (j + 1) & 1);
+        cp_async_wait<STG - 2>();
+        __syncwarp();  // every lane has read chunk j - 1: its buffer takes chunk j + STG - 1
+        if (j + STG - 1 < nin)
+          issue(j + STG - 1, sbuf == 0 ? STG - 1 : sbuf - 1);
+        else
+          cp_async_commit();
         if (j >= NSLOT) {  // ring slot of chunk j last served output chunk j - NSLOT
           const uint32_t go = out_ctr + (j - NSLOT);
           mbar_wait(&bar_done[go % NSLOT], (go / NSLOT) & 1);
         }
-        const unsigned char* cur = mystage + (j & 1) * 8 * rowbytes;
+        const unsigned char* cur = mystage + sbuf * 8 * rowbytes;
+        sbuf = sbuf + 1 == STG ? 0 : sbuf + 1;
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
           const int rr = lane & 7, sc = (lane >> 3) + 4 * pass;
@@ -2021,32 +2225,35 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
       }
       report_status(status, bad, t);
     } else {
-      const int c = threadIdx.x;
-      int* midrow[HB];  // destination rows of this band - hoisted
-#pragma unroll
-      for (int r = 0; r < HB; ++r) {
+      const int c = threadIdx.x & (CW - 1);
+      const int r0 = (threadIdx.x / CW) * SHB;  // this thread's rows [r0, r0 + SHB) of the band
+      // destination of tall row t: a full band inside one image is HB rows one plane row apart
+      // (one pointer stepped by the row stride); other bands address every row
+      auto midrow_of = [&](int r) {
         const long long trow = row0 + min(r, nrows - 1);
         const int img = (int)(trow / g.H), v = (int)(trow - (long long)img * g.H);
-        midrow[r] = mid_out + ch * g.mid_ch + (long long)img * g.mid_img + (long long)v * g.mid_row;
-      }
+        return mid_out + ch * g.mid_ch + (long long)img * g.mid_img + (long long)v * g.mid_row;
+      };
+      const bool whole = nrows == HB && (row0 / g.H) == ((row0 + HB - 1) / g.H);
+      const size_t mid0g = __cvta_generic_to_global(midrow_of(r0));
       // two output chunks per iteration: one wait (chunks complete in order), both chunks'
       // row values in flight together, then both done-arrivals and stores
       for (int o = 0; o < nout; o += 2) {
         const int no = min(2, nout - o);
         const uint32_t gj = cin_ctr + min(o + no - 1 + lagc, nin - 1);
         mbar_wait(&bar_full[gj % NSLOT], (gj / NSLOT) & 1);
-        float2 rv[2][HB / 2];  // rows (2r, 2r+1) of chunks o, o+1: packed FMUL2 / FFMA2 / FADD2
+        float2 rv[2][SHB / 2];  // rows r0 + (2r, 2r+1) of chunks o, o+1: packed FMUL2 / FFMA2 / FADD2
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h >= no) break;
           const int x = (o + h) * CW + c;
 #pragma unroll
           for (int i = 0; i < K; ++i) {
-            const int* pl = P + ((x - xs + t.p[i]) & (RL - 1));
-            const int* pt = P + ((x - xs - t.p[i] - 1) & (RL - 1));
+            const int* pl = P + r0 * RLS + ((x - xs + t.p[i]) & (RL - 1));
+            const int* pt = P + r0 * RLS + ((x - xs - t.p[i] - 1) & (RL - 1));
             const float2 w2 = make_float2(t.w_row[i], t.w_row[i]);
 #pragma unroll
-            for (int r = 0; r < HB / 2; ++r) {
+            for (int r = 0; r < SHB / 2; ++r) {
               const float2 d = make_float2(i2f_fast((uint32_t)(pl[2 * r * RLS] - pt[2 * r * RLS])),
                                            i2f_fast((uint32_t)(pl[(2 * r + 1) * RLS] - pt[(2 * r + 1) * RLS])));
               rv[h][r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, rv[h][r]);
@@ -2064,11 +2271,25 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
           if (h >= no) break;
           const int x = (o + h) * CW + c;
           if (x < g.W) {
+            if (whole) {
+              // 32-bit element offsets from the band's first row (HB plane rows < 2^31 elements):
+              // one IMAD.WIDE per store instead of a 64-bit pointer chain
+              const int ms = (int)g.mid_row;
+              int idx = x;
 #pragma unroll
-            for (int r = 0; r < HB / 2; ++r) {
-              const float2 q = round_mid2<K>(rv[h][r]);  // round to the mid quantum
-              if (2 * r < nrows) midrow[2 * r][x] = __float_as_int(q.x) - kMagicBits;
-              if (2 * r + 1 < nrows) midrow[2 * r + 1][x] = __float_as_int(q.y) - kMagicBits;
+              for (int r = 0; r < SHB / 2; ++r) {
+                const float2 q = round_mid2<K>(rv[h][r]);  // round to the mid quantum
+                st_global_idx(mid0g, idx, __float_as_int(q.x) - kMagicBits);
+                st_global_idx(mid0g, idx + ms, __float_as_int(q.y) - kMagicBits);
+                idx += 2 * ms;
+              }
+            } else {
+#pragma unroll
+              for (int r = 0; r < SHB / 2; ++r) {
+                const float2 q = round_mid2<K>(rv[h][r]);
+                if (r0 + 2 * r < nrows) midrow_of(r0 + 2 * r)[x] = __float_as_int(q.x) - kMagicBits;
+                if (r0 + 2 * r + 1 < nrows) midrow_of(r0 + 2 * r + 1)[x] = __float_as_int(q.y) - kMagicBits;
+              }
             }
           }
         }
@@ -2080,7 +2301,8 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2)
   }
 }
 
-inline const void* stream_ptr_for_f32(int k) {
+template <typename Unused = void>  // a template: instantiates its kernels only where it is called
+const void* stream_ptr_for_f32(int k) {
 #define SB_STREAM(KK) stream_rows_kernel<float, KK>
   switch (k) {
     case 1: return (const void*)SB_STREAM(1);
@@ -2118,6 +2340,7 @@ const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)
 const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
 const void* sweep_ptr_fused5(int k);      // fused sweep, two bands per consumer iteration (uint8, one channel)
+const void* sweep_ptr_fusedp(int k);      // fused sweep, paired consumer warps (uint8, one channel)
 const void* sweep_ptr_fused_f32(int k, int ls);  // fused sweep of float32 sources with prefix stride ls
 const void* sweep_ptr_fusedw(int k, int lsw);    // wide fused sweep (sweep_wide.cu), slot stride lsw
 const void* sweep_ptr_rowtile(int k);            // uint8 row-tile sweep (sweep_rowtile.cu)
@@ -2157,13 +2380,15 @@ inline const void* fused_f32_ptr_for(int k) {
 #undef SB_FF
 }
 
-inline const void* cols_ptr_for(int k) {
+template <typename Unused = void>  // a template: instantiates its kernels only where it is called
+const void* cols_ptr_for(int k) {
 #define SB_COLS(KK) cols_kernel<KK>
   SB_K_CASES(SB_COLS)
 #undef SB_COLS
 }
 
-inline const void* cols2_ptr_for(int k) {
+template <typename Unused = void>  // a template: instantiates its kernels only where it is called
+const void* cols2_ptr_for(int k) {
 #define SB_COLS2(KK) cols2_kernel<KK>
   SB_K_CASES(SB_COLS2)
 #undef SB_COLS2

@@ -119,7 +119,7 @@ def test_paths_bit_identical(name, dtype, shape, ch, k, sigma):
     np.testing.assert_array_equal(outs[nat.SB_PATH_AUTO], outs[nat.SB_PATH_GENERIC])
     np.testing.assert_array_equal(outs[nat.SB_PATH_AUTO], outs[nat.SB_PATH_UNFUSED])
     if dtype == np.uint8:
-        for pol in (nat.SB_PATH_U8_THREE_CTA, nat.SB_PATH_U8_ONE_BAND):
+        for pol in (nat.SB_PATH_U8_THREE_CTA, nat.SB_PATH_U8_ONE_BAND, nat.SB_PATH_U8_PAIRED, nat.SB_PATH_U8_TWO_BAND):
             with nat.path_policy(pol):
                 got = F.separable_filter_batch(x, kern).cpu().numpy()
             np.testing.assert_array_equal(outs[nat.SB_PATH_AUTO], got)

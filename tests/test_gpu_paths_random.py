@@ -59,7 +59,8 @@ def test_every_policy_bit_identical(seed):
             return F.separable_filter_batch(x, kern, channels_last=ch > 1, value_bound=bound).cpu().numpy()
 
     base = run(nat.SB_PATH_AUTO)
-    policies = [nat.SB_PATH_GENERIC, nat.SB_PATH_UNFUSED, nat.SB_PATH_FUSED_WIDE, nat.SB_PATH_U8_ROWTILE]
+    policies = [nat.SB_PATH_GENERIC, nat.SB_PATH_UNFUSED, nat.SB_PATH_FUSED_WIDE, nat.SB_PATH_U8_ROWTILE,
+                nat.SB_PATH_U8_PAIRED, nat.SB_PATH_U8_TWO_BAND]
     for pol in policies:
         np.testing.assert_array_equal(run(pol), base, err_msg=f"policy {pol} seed {seed}")
     gabs = float(np.sum(np.abs(kern.weights) * (2 * kern.radii + 1)))
@@ -106,7 +107,8 @@ def test_windows_rows_and_wide_radii_bit_identical(seed):
         return a, b
 
     base_w, base_r = run(nat.SB_PATH_AUTO)
-    for pol in (nat.SB_PATH_GENERIC, nat.SB_PATH_UNFUSED, nat.SB_PATH_FUSED_WIDE, nat.SB_PATH_U8_ROWTILE):
+    for pol in (nat.SB_PATH_GENERIC, nat.SB_PATH_UNFUSED, nat.SB_PATH_FUSED_WIDE, nat.SB_PATH_U8_ROWTILE,
+                nat.SB_PATH_U8_PAIRED, nat.SB_PATH_U8_TWO_BAND):
         got_w, got_r = run(pol)
         np.testing.assert_array_equal(got_w, base_w, err_msg=f"window, policy {pol} seed {seed}")
         np.testing.assert_array_equal(got_r, base_r, err_msg=f"rows, policy {pol} seed {seed}")

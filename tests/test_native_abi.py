@@ -173,4 +173,4 @@ def test_one_launch_routing_per_policy(lib):
     with nat.path_policy(nat.SB_PATH_U8_ROWTILE):
         for p in (0, 7, 23, 100):
             assert ws(nat.SB_DTYPE_U8, p) == 0, p
-    assert lib.sb_set_path_policy(nat.SB_PATH_U8_ROWTILE + 1) == -1
+    assert lib.sb_set_path_policy(nat.SB_PATH_U8_TWO_BAND + 1) == -1

@@ -39,8 +39,8 @@ def main():
         g = torch.Generator(device="cuda").manual_seed(1)
         x = torch.randint(0, 256, (n, h, w), device="cuda", generator=g, dtype=torch.uint8)
         res = {}
-        for name, pol in (("rowtile", nat.SB_PATH_U8_ROWTILE), ("fused2", nat.SB_PATH_AUTO),
-                          ("fused3", nat.SB_PATH_U8_THREE_CTA)):
+        for name, pol in (("paired", nat.SB_PATH_U8_PAIRED), ("fused2", nat.SB_PATH_U8_TWO_BAND),
+                          ("fused3", nat.SB_PATH_U8_THREE_CTA), ("rowtile", nat.SB_PATH_U8_ROWTILE)):
             out = torch.empty((n, h, w), device="cuda", dtype=torch.float32)
             with nat.path_policy(pol):
                 t = timed(x, kern, out, iters)
