@@ -313,6 +313,9 @@ const void* pick_kernel(sb::Mode m, int dtype, int k) {
 #define SB_COLS2_SMEM_KB 224
 #endif
 constexpr size_t kCols2Smem = (size_t)SB_COLS2_SMEM_KB * 1024;
+#ifndef SB_STREAM_MC
+#define SB_STREAM_MC 1
+#endif
 #ifndef SB_COLS2_MINPF
 #define SB_COLS2_MINPF 2
 #endif
@@ -971,21 +974,27 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
   if (route.rows == RowPath::Stream) {
     // streaming row pass: full-width bands, prefix carried across chunks
     const int xs = -(((plan.pmax + 1) + 15) & ~15);  // first halo column, 16-aligned
-    const void* fs = sb::sweep_ptr_stream_f32(k);
-    const size_t smem = (size_t)sb::NPROD * sb::STG * 8 * (sb::CW * sizeof(float) + sb::SRB_PAD) +
-                        (size_t)sb::HB * sb::RLS * sizeof(int);
+    // interleaved channels with 16-byte aligned rows: bands of virtual (row, channel) rows, the
+    // image rows staged once for all channels (stream_rows_mc_kernel); else one channel per CTA
+    const bool mc = SB_STREAM_MC && channels >= 2 && channels <= 4 && g.in_px == channels && g.aligned16 &&
+                    (width * channels) % 4 == 0 && all_rows * width * channels < (1LL << 31);
+    const void* fs = mc ? sb::sweep_ptr_stream_mc(k) : sb::sweep_ptr_stream_f32(k);
+    const size_t stage = mc ? (size_t)sb::STG * sb::mc_rows(channels) * (sb::CW * channels * sizeof(float) + sb::SRB_PAD)
+                            : (size_t)sb::NPROD * sb::STG * 8 * (sb::CW * sizeof(float) + sb::SRB_PAD);
+    const size_t smem = stage + (size_t)sb::HB * sb::RLS * sizeof(int);
     FnFacts ff;
     DevFacts df;
     rc = launch_facts(fs, smem, &ff, &df);
     if (rc) return rc;
-    const int nb_total = (int)((all_rows + sb::HB - 1) / sb::HB);
-    const int gx = std::max(1, std::min(nb_total, df.sms * 2 * 8 / std::max(1, channels)));
+    const int nb_total = (int)(((mc ? all_rows * channels : all_rows) + sb::HB - 1) / sb::HB);
+    const int gx = mc ? std::max(1, std::min(nb_total, df.sms * 2 * 8))
+                      : std::max(1, std::min(nb_total, df.sms * 2 * 8 / std::max(1, channels)));
     void* args[] = {(void*)&src, (void*)&mid, (void*)&g, (void*)&plan.taps, (void*)&xs, (void*)&nb_total,
                     (void*)&status_dev};
     if (debug_plans())
       std::fprintf(stderr, "[sliceblur_b200] stream rows: pmax=%d xs=%d bands=%d grid=%d x %d smem=%zu\n",
                    plan.pmax, xs, nb_total, gx, channels, smem);
-    cudaError_t e = cudaLaunchKernel(fs, dim3(gx * channels, 1), dim3(sb::STREAM_THREADS), args, smem, st);
+    cudaError_t e = cudaLaunchKernel(fs, dim3(mc ? gx : gx * channels, 1), dim3(sb::STREAM_THREADS), args, smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
   } else if (route.rows == RowPath::Tiled) {
     const void* f1 = pick_kernel(sb::Mode::RowsToMid, src_dtype, k);

@@ -2301,6 +2301,215 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
   }
 }
 
+// ---------------------------------------------------------------- streaming row pass, interleaved channels
+// float32 sources with C = 2..4 interleaved channels and 16-byte aligned rows (C4).  The band
+// is HB VIRTUAL rows vr = t * C + ch (tall row t, channel ch), so a band touches at most
+// HB / C + 2 image rows.  The two producer warps stage those rows ONCE per chunk, interleaved
+// as they lie in memory (16-byte cp.async; the per-element 4-byte gather of
+// stream_rows_kernel left the consumers waiting for the producers 58 % of the time on C4),
+// and each scan lane reads its channel out of the staged row with stride C.  Prefix ring,
+// consumers and hand-offs are those of stream_rows_kernel; the int32 plane is
+// [channel][tall row][W], dense, below 2^31 elements (32-bit store offsets).
+constexpr int mc_rows(int C) { return (HB + C - 1) / C + 1; }
+
+template <int K>
+__global__ void __launch_bounds__(STREAM_THREADS, 2)
+    stream_rows_mc_kernel(const float* __restrict__ src, int* __restrict__ mid_out, Geometry g, Taps t, int xs,
+                          int nbands_total, int* status) {
+  static_assert(SRG == 1, "the interleaved streaming row pass assumes one consumer row group");
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
+  __shared__ const float* rowp_s[HB / 2 + 2];  // the band's image rows (clamped at the end of the tall image)
+  const int warp = threadIdx.x >> 5;
+  const bool producer = warp >= SCONS;
+  const int C = g.in_px;
+  const int qtotal = g.W - xs + t.pmax;
+  const int nin = (qtotal + CW - 1) / CW;
+  const int nout = (g.W + CW - 1) / CW;
+  const int lagc = (CW - 1 - xs + t.pmax) / CW;
+  const int ntmax = (HB + C - 1) / C + 1;
+  const int srb = CW * C * 4 + SRB_PAD;       // staged image row: CW pixels of C floats (+ 16: odd multiple of 16)
+  unsigned char* stage = smem;                // [STG][ntmax][srb]
+  int* P = (int*)(smem + STG * ntmax * srb);  // [HB][RLS]
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSLOT; ++i) {
+      mbar_init(&bar_full[i], 32 * NPROD);
+      mbar_init(&bar_done[i], 32 * SCONS);
+    }
+  }
+  __syncthreads();
+
+  const long long tall = (long long)g.nimg * g.H;
+  const long long VR = tall * C;  // virtual rows
+  uint32_t cin_ctr = 0, out_ctr = 0;
+  for (int band = blockIdx.x; band < nbands_total; band += gridDim.x) {
+    const long long vr0 = (long long)band * HB;
+    const int nrows = (int)min((long long)HB, VR - vr0);
+    const long long t_first = vr0 / C;
+    const int c_first = (int)(vr0 - t_first * C);
+    const int nt = (int)((vr0 + nrows - 1) / C - t_first) + 1;  // image rows of this band
+    if (producer) {
+      const int lane = threadIdx.x & 31, pw = warp - SCONS, ptid = pw * 32 + lane;
+      if (ptid < nt) {
+        const long long tt = t_first + ptid;
+        const int img = (int)(tt / g.H), v = (int)(tt - (long long)img * g.H);
+        rowp_s[ptid] = src + (long long)img * g.in_img + (long long)v * g.in_row;
+      }
+      named_bar_sync(1, 32 * NPROD);
+      auto issue = [&](int j, int buf) {
+        const int xq0 = xs + j * CW;  // 16-aligned first column of chunk j
+        unsigned char* sbuf = stage + buf * ntmax * srb;
+        if (xq0 >= 0 && xq0 + CW <= g.W) {
+          const int nvec = CW * C / 4;  // 16-byte vectors per staged row
+          for (int i = 0; i < nt; ++i) {
+            const float* rp = rowp_s[i] + (long long)xq0 * C;
+            for (int e = ptid; e < nvec; e += 32 * NPROD) cp_async16(sbuf + i * srb + 16 * e, rp + 4 * e);
+          }
+        } else {
+          // edge chunk: element copies, border columns replicated (filtering.py:10-13)
+          for (int i = 0; i < nt; ++i) {
+            const float* rp = rowp_s[i];
+            for (int e = ptid; e < CW * C; e += 32 * NPROD) {
+              const int px = e / C, cc = e - px * C;
+              const int x = min(max(xq0 + px, 0), g.W - 1);
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(sbuf + i * srb + 4 * e)),
+                           "l"(rp + (long long)x * C + cc));
+            }
+          }
+        }
+        cp_async_commit();
+      };
+      // this lane's virtual row: band row 8 pw + rr (clamped), channel cc of staged image row srow
+      const int rr = lane & 7;
+      const long long vr = vr0 + min(8 * pw + rr, nrows - 1);
+      const long long tt = vr / C;
+      const int lane_off = (int)(tt - t_first) * srb + (int)(vr - tt * C) * 4;
+      int carry = 0;
+#pragma unroll
+      for (int j = 0; j < STG - 1; ++j) {
+        if (j < nin)
+          issue(j, j);
+        else
+          cp_async_commit();
+      }
+      RangeAcc bad;
+      int sb = 0;  // j % STG
+      for (int j = 0; j < nin; ++j) {
+        const uint32_t gj = cin_ctr + j;
+        cp_async_wait<STG - 2>();
+        // both warps' copies of chunk j have landed, and both have read chunk j - 1 (its buffer
+        // takes chunk j + STG - 1)
+        named_bar_sync(1, 32 * NPROD);
+        if (j + STG - 1 < nin)
+          issue(j + STG - 1, sb == 0 ? STG - 1 : sb - 1);
+        else
+          cp_async_commit();
+        if (j >= NSLOT) {
+          const uint32_t go = out_ctr + (j - NSLOT);
+          mbar_wait(&bar_done[go % NSLOT], (go / NSLOT) & 1);
+        }
+        const unsigned char* cur = stage + sb * ntmax * srb + lane_off;
+        sb = sb + 1 == STG ? 0 : sb + 1;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          const int sc = (lane >> 3) + 4 * pass;
+          const float* e = (const float*)cur + sc * CH * C;
+          int v[CH];
+          int tot = 0;
+#pragma unroll
+          for (int m = 0; m < CH; ++m) {
+            tot += to_fixed<float>(e[m * C], t, bad);
+            v[m] = tot;
+          }
+          int inc = tot;
+          int y = __shfl_up_sync(0xffffffffu, inc, 8);
+          if (lane >= 8) inc += y;
+          y = __shfl_up_sync(0xffffffffu, inc, 16);
+          if (lane >= 16) inc += y;
+          const int off = carry + inc - tot;
+          int* dst = P + (8 * pw + rr) * RLS + ((j * CW + sc * CH) & (RL - 1));
+#pragma unroll
+          for (int m = 0; m < CH / 4; ++m)
+            ((int4*)dst)[m] = make_int4(v[4 * m] + off, v[4 * m + 1] + off, v[4 * m + 2] + off, v[4 * m + 3] + off);
+          carry += __shfl_sync(0xffffffffu, inc, rr + 24);
+        }
+        mbar_arrive(&bar_full[gj % NSLOT]);
+      }
+      report_status(status, bad, t);
+    } else {
+      const int c = threadIdx.x;
+      const size_t midg = __cvta_generic_to_global(mid_out);
+      const int off0 = (int)((long long)c_first * g.mid_ch + t_first * g.mid_row);  // plane offset of band row 0
+      const int ch_step = (int)g.mid_ch, wrap_step = (int)(g.mid_row - (long long)C * g.mid_ch);
+      for (int o = 0; o < nout; o += 2) {
+        const int no = min(2, nout - o);
+        const uint32_t gj = cin_ctr + min(o + no - 1 + lagc, nin - 1);
+        mbar_wait(&bar_full[gj % NSLOT], (gj / NSLOT) & 1);
+        float2 rv[2][HB / 2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h >= no) break;
+          const int x = (o + h) * CW + c;
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            const int* pl = P + ((x - xs + t.p[i]) & (RL - 1));
+            const int* pt = P + ((x - xs - t.p[i] - 1) & (RL - 1));
+            const float2 w2 = make_float2(t.w_row[i], t.w_row[i]);
+#pragma unroll
+            for (int r = 0; r < HB / 2; ++r) {
+              const float2 d = make_float2(i2f_fast((uint32_t)(pl[2 * r * RLS] - pt[2 * r * RLS])),
+                                           i2f_fast((uint32_t)(pl[(2 * r + 1) * RLS] - pt[(2 * r + 1) * RLS])));
+              rv[h][r] = i == 0 ? __fmul2_rn(w2, d) : __ffma2_rn(w2, d, rv[h][r]);
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h >= no) break;
+          const uint32_t go = out_ctr + o + h;
+          mbar_arrive(&bar_done[go % NSLOT]);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h >= no) break;
+          const int x = (o + h) * CW + c;
+          if (x < g.W) {
+            int off = off0 + x, cc = c_first;
+#pragma unroll
+            for (int r = 0; r < HB / 2; ++r) {
+              const float2 q = round_mid2<K>(rv[h][r]);  // round to the mid quantum
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                if (2 * r + u < nrows) st_global_idx(midg, off, __float_as_int(u ? q.y : q.x) - kMagicBits);
+                ++cc;
+                off += cc == C ? wrap_step + ch_step : ch_step;
+                cc = cc == C ? 0 : cc;
+              }
+            }
+          }
+        }
+      }
+    }
+    cin_ctr += (uint32_t)nin;
+    out_ctr += (uint32_t)nout;
+    __syncthreads();  // the next band restarts the ring, the carries and the row pointers
+  }
+}
+
+template <typename Unused = void>
+const void* stream_mc_ptr_for(int k) {
+  switch (k) {
+    case 1: return (const void*)stream_rows_mc_kernel<1>;
+    case 2: return (const void*)stream_rows_mc_kernel<2>;
+    case 3: return (const void*)stream_rows_mc_kernel<3>;
+    case 4: return (const void*)stream_rows_mc_kernel<4>;
+    case 5: return (const void*)stream_rows_mc_kernel<5>;
+    case 6: return (const void*)stream_rows_mc_kernel<6>;
+    case 7: return (const void*)stream_rows_mc_kernel<7>;
+    default: return (const void*)stream_rows_mc_kernel<8>;
+  }
+}
+
 template <typename Unused = void>  // a template: instantiates its kernels only where it is called
 const void* stream_ptr_for_f32(int k) {
 #define SB_STREAM(KK) stream_rows_kernel<float, KK>
@@ -2338,6 +2547,7 @@ int launch_cols_generic(void* mid, float* dst, const Geometry& g, const TapsG& t
 const void* sweep_ptr_cols(int k);   // ColsFromMid (source type unused)
 const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)
+const void* sweep_ptr_stream_mc(int k);   // streaming row pass, interleaved float32 channels staged once
 const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
 const void* sweep_ptr_fused5(int k);      // fused sweep, two bands per consumer iteration (uint8, one channel)
 const void* sweep_ptr_fusedp(int k);      // fused sweep, paired consumer warps (uint8, one channel)
