@@ -205,6 +205,13 @@ __device__ __forceinline__ void tma_load_3d(void* sdst, const CUtensorMap* map, 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// bulk copy global -> shared (bytes and both addresses multiples of 16), completion on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -2319,7 +2326,8 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
   static_assert(SRG == 1, "the interleaved streaming row pass assumes one consumer row group");
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
-  __shared__ const float* rowp_s[HB / 2 + 2];  // the band's image rows (clamped at the end of the tall image)
+  __shared__ __align__(8) uint64_t sfull[STG];  // staged chunk landed (bulk-copy bytes / edge-chunk arrive)
+  __shared__ const float* rowp_s[HB / 2 + 2];   // the band's image rows (clamped at the end of the tall image)
   const int warp = threadIdx.x >> 5;
   const bool producer = warp >= SCONS;
   const int C = g.in_px;
@@ -2336,6 +2344,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
       mbar_init(&bar_full[i], 32 * NPROD);
       mbar_init(&bar_done[i], 32 * SCONS);
     }
+    for (int i = 0; i < STG; ++i) mbar_init(&sfull[i], 1);
   }
   __syncthreads();
 
@@ -2356,17 +2365,26 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
         rowp_s[ptid] = src + (long long)img * g.in_img + (long long)v * g.in_row;
       }
       named_bar_sync(1, 32 * NPROD);
-      auto issue = [&](int j, int buf) {
+      // Chunk gc (counted over the CTA's bands) lives in staging buffer gc % STG; its landing is
+      // phase gc / STG of sfull[gc % STG].  Interior chunks: one bulk copy per image row, issued
+      // by one thread (expect_tx + complete_tx).  Edge chunks (border columns replicated,
+      // filtering.py:10-13): 4-byte cp.async by all producer threads, waited for as a group; the
+      // issuing thread completes the phase by a plain arrive so every buffer use is one phase.
+      auto interior = [&](int j) {
         const int xq0 = xs + j * CW;  // 16-aligned first column of chunk j
+        return xq0 >= 0 && xq0 + CW <= g.W;
+      };
+      auto issue = [&](int j) {
+        const int xq0 = xs + j * CW;
+        const int buf = (int)((cin_ctr + (uint32_t)j) % STG);
         unsigned char* sbuf = stage + buf * ntmax * srb;
-        if (xq0 >= 0 && xq0 + CW <= g.W) {
-          const int nvec = CW * C / 4;  // 16-byte vectors per staged row
-          for (int i = 0; i < nt; ++i) {
-            const float* rp = rowp_s[i] + (long long)xq0 * C;
-            for (int e = ptid; e < nvec; e += 32 * NPROD) cp_async16(sbuf + i * srb + 16 * e, rp + 4 * e);
+        if (interior(j)) {
+          if (ptid == 0) {
+            mbar_expect_tx(&sfull[buf], (uint32_t)(nt * CW * C * 4));
+            for (int i = 0; i < nt; ++i)
+              bulk_g2s(sbuf + i * srb, rowp_s[i] + (long long)xq0 * C, (uint32_t)(CW * C * 4), &sfull[buf]);
           }
         } else {
-          // edge chunk: element copies, border columns replicated (filtering.py:10-13)
           for (int i = 0; i < nt; ++i) {
             const float* rp = rowp_s[i];
             for (int e = ptid; e < CW * C; e += 32 * NPROD) {
@@ -2376,8 +2394,9 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
                            "l"(rp + (long long)x * C + cc));
             }
           }
+          cp_async_commit();
+          if (ptid == 0) mbar_arrive(&sfull[buf]);
         }
-        cp_async_commit();
       };
       // this lane's virtual row: band row 8 pw + rr (clamped), channel cc of staged image row srow
       const int rr = lane & 7;
@@ -2385,31 +2404,22 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
       const long long tt = vr / C;
       const int lane_off = (int)(tt - t_first) * srb + (int)(vr - tt * C) * 4;
       int carry = 0;
-#pragma unroll
-      for (int j = 0; j < STG - 1; ++j) {
-        if (j < nin)
-          issue(j, j);
-        else
-          cp_async_commit();
-      }
+      for (int j = 0; j < STG - 1 && j < nin; ++j) issue(j);
       RangeAcc bad;
-      int sb = 0;  // j % STG
       for (int j = 0; j < nin; ++j) {
         const uint32_t gj = cin_ctr + j;
-        cp_async_wait<STG - 2>();
-        // both warps' copies of chunk j have landed, and both have read chunk j - 1 (its buffer
-        // takes chunk j + STG - 1)
+        const int sb = (int)(gj % STG);
+        if (!interior(j)) cp_async_wait_all();
+        mbar_wait(&sfull[sb], (gj / STG) & 1);
+        // both warps have read chunk j - 1 (its buffer takes chunk j + STG - 1), and an edge
+        // chunk's copies by the other warp are visible
         named_bar_sync(1, 32 * NPROD);
-        if (j + STG - 1 < nin)
-          issue(j + STG - 1, sb == 0 ? STG - 1 : sb - 1);
-        else
-          cp_async_commit();
+        if (j + STG - 1 < nin) issue(j + STG - 1);
         if (j >= NSLOT) {
           const uint32_t go = out_ctr + (j - NSLOT);
           mbar_wait(&bar_done[go % NSLOT], (go / NSLOT) & 1);
         }
         const unsigned char* cur = stage + sb * ntmax * srb + lane_off;
-        sb = sb + 1 == STG ? 0 : sb + 1;
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
           const int sc = (lane >> 3) + 4 * pass;

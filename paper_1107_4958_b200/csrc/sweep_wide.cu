@@ -27,12 +27,6 @@
 
 namespace sb {
 
-__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(sdst)),
-               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 
 // In-place prefix scan of rows r0 .. r0+3 (those < n) of a slot: float32 elements ->
 // inclusive int32 prefixes in the input quantum (to_fixed).  Lane (rr, cq) = (lane & 3,
