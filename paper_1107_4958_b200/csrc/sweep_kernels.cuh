@@ -1796,8 +1796,12 @@ __global__ void __launch_bounds__(C2THREADS, 1)
                  const __grid_constant__ CUtensorMap omap, const __grid_constant__ CUtensorMap mmap) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_base_s;
-  __shared__ __align__(8) uint64_t done[C2DONE], lfull[C2PF], lempty[C2PF];
+  __shared__ __align__(8) uint64_t lfull[C2PF], lempty[C2PF];
   __shared__ uint32_t ring_cnt[4];  // ring bands written, per lane quadrant (monotonic: cannot alias)
+  // output bands finished by output group g in lane quadrant q (monotonic).  The loader of a
+  // quadrant waits only for the three output warps that read its TMEM lanes: one ld.acquire per
+  // output band instead of an mbarrier all four quadrants arrive on.
+  __shared__ uint32_t out_cnt[4][CG];
   const int ch = blockIdx.x % g.in_px;
   const int sidx = blockIdx.x / g.in_px;
   const int strip = sidx % tl.nstrips;
@@ -1818,7 +1822,7 @@ __global__ void __launch_bounds__(C2THREADS, 1)
   float* obuf = (float*)(abase + tl.obuf_off);
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) ring_cnt[i] = 0;
-    for (int i = 0; i < C2DONE; ++i) mbar_init(&done[i], 32 * 4);
+    for (int i = 0; i < 4 * CG; ++i) (&out_cnt[0][0])[i] = 0;
     for (int i = 0; i < PF; ++i) {
       mbar_init(&lfull[i], 1);   // the issuing thread's expect_tx + the TMA bytes
       mbar_init(&lempty[i], 4);  // one arrive per loader warp
@@ -1836,8 +1840,9 @@ __global__ void __launch_bounds__(C2THREADS, 1)
     sc.init(T0, T1, wh, g.oy0, t.pmax);
     so.init(T0, T1, wh, g.oy0, t.pmax);
     uint32_t v = 0;  // global ring band
-    uint32_t onum = 0;
-    int oob = 0;     // next output band to observe: index onum, band oob of segment so
+    int og = 0;         // next output band to observe: the ocnt-th band of output group og,
+    uint32_t ocnt = 0;  // band oob of segment so
+    int oob = 0;
     int slot = 0;
     // plane bands arrive in pairs by TMA (one 32 x 128 box, issued PF-1 pairs ahead by
     // thread 0) into PF slots with full (tx bytes) / empty (one arrive per warp) barriers;
@@ -1869,13 +1874,17 @@ __global__ void __launch_bounds__(C2THREADS, 1)
         const int nbp = min(2, sc.nbands - 2 * pp);  // bands in this pair
         // every output band reading ring bands v+d - NB from TMEM is done
         while (so.valid && (long long)(so.gb0 + (uint32_t)oob) + tl.lag <= (long long)v + nbp - 1) {
-          mbar_wait(&done[onum % C2DONE], (onum / C2DONE) & 1);
-          ++onum;
+          wait_above(&out_cnt[q][og], ocnt, false);
+          if (++og == CG) {
+            og = 0;
+            ++ocnt;
+          }
           if (++oob == (so.b - so.a + HB - 1) / HB) {
             so.next();
             oob = 0;
           }
         }
+        tmem_fence_after();  // the ring stores below are ordered after the readers' release
         uint32_t cv[2][HB];
         mbar_wait(&lfull[lslot], lph);
 #pragma unroll
@@ -2030,8 +2039,11 @@ __global__ void __launch_bounds__(C2THREADS, 1)
           }
         }
         }
+        // this warp's windows of the band are read (tcgen05.wait::ld above): the loader may
+        // overwrite the ring bands only this band still needed
         tmem_fence_before();
-        mbar_arrive(&done[onum % C2DONE]);
+        __syncwarp();
+        if (lane == 0) st_release(&out_cnt[q][grp], onum / CG + 1);
         if (g.out_bulk && nb == HB) {
           float* obp = obuf + (ow * 2 + obsel) * (HB * 32);
           if (lane == 0) bulk_wait_read<1>();
