@@ -629,7 +629,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // Output tensor map [image][row][column] (fp32) with a 16 x 32 box: one box per
 // consumer warp and output band.  Clears g.out_bulk when no map can be made.
-void make_output_map(float* dst, sb::Geometry& g, CUtensorMap* map) {
+void make_output_map(float* dst, sb::Geometry& g, CUtensorMap* map, int box_rows = sb::HB) {
   std::memset(map, 0, sizeof(*map));
   if (!g.out_bulk) return;
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
@@ -638,7 +638,7 @@ void make_output_map(float* dst, sb::Geometry& g, CUtensorMap* map) {
   const cuuint64_t rstride = (cuuint64_t)g.out_row * 4;
   const cuuint64_t istride = g.nimg > 1 ? (cuuint64_t)g.out_img * 4 : rstride * (cuuint64_t)rows;
   const cuuint64_t strides[2] = {rstride, istride};
-  const cuuint32_t box[3] = {32, (cuuint32_t)sb::HB, 1};
+  const cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   if (!enc || enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)dst, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,

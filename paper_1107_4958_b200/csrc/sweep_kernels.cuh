@@ -1406,7 +1406,7 @@ __global__ void __launch_bounds__(PAIRED ? PTHREADS : FTHREADS, MINB)
         int produced = 0;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          if (pb + h < nbands) {
+          if (h == 0 || pb + h < nbands) {  // the first band of a turn always exists
             const uint32_t kb = gb / FPROD;
             const int pbi = (int)(gb % FPROD) * tl.npb + (int)(kb & (uint32_t)(tl.npb - 1));
             const float2* P = (const float2*)(Pbase + pbi * pbuf_words);
