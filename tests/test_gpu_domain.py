@@ -235,3 +235,30 @@ def test_pipelined_host_batch_float_single_status():
     bad[4, 10, 10] = float("nan")
     with pytest.raises(ValueError):
         F.separable_filter_batch(bad, kern, out=out_host)
+
+
+# The interleaved-channel streaming row pass (stream_rows_mc_kernel): bands of virtual
+# (row, channel) rows that straddle image rows and images, 2..4 channels, a partial last
+# band, edge chunks on both sides, and the fall-back when W * C is not a multiple of 4.
+@pytest.mark.parametrize("shape,k,sigma", [
+    ((2, 37, 260, 2), 4, 8.0),    # two channels, two images: bands straddle the image boundary
+    ((3, 50, 300, 4), 5, 12.0),   # four channels
+    ((1, 333, 516, 3), 4, 64.0),  # three channels, odd height (partial last band), p_max 164
+    ((5, 13, 388, 3), 3, 5.0),    # images shorter than a band: a band covers several images
+    ((1, 40, 301, 3), 4, 8.0),    # W * C not a multiple of 4: one channel per CTA (stream_rows_kernel)
+], ids=["c2-two-images", "c4", "c3-odd-height", "c3-short-images", "c3-unaligned-fallback"])
+def test_interleaved_channels_streaming_rows(shape, k, sigma):
+    rng = np.random.default_rng(sum(shape))
+    x = (rng.random(shape) * 255).astype(np.float32)
+    kern = A.table_kernel(k, sigma)
+    assert kern.max_radius < min(shape[1], shape[2])
+    xt = torch.from_numpy(x).cuda()
+    with nat.path_policy(nat.SB_PATH_UNFUSED):  # small radii would take the fused sweep otherwise
+        got = F.separable_filter_batch(xt, kern, channels_last=True, value_bound=255.0).cpu().numpy()
+    with nat.path_policy(nat.SB_PATH_GENERIC):
+        gen = F.separable_filter_batch(xt, kern, channels_last=True, value_bound=255.0).cpu().numpy()
+    np.testing.assert_array_equal(got, gen)  # bit-identical to the generic kernels
+    for n in range(shape[0]):
+        for c in range(shape[3]):
+            ref = O.separable_filter_2d(np.ascontiguousarray(x[n, :, :, c]), kern.radii, kern.weights)
+            assert float(np.abs(got[n, :, :, c] - ref).max()) <= BAR
