@@ -1095,6 +1095,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define SB_WD_CHECK(what, a, b)
 #endif
 
+#ifndef SB_WA_MAXNS
+#define SB_WA_MAXNS 256
+#endif
 // wait until *p > v
 __device__ __forceinline__ void wait_above(const uint32_t* p, uint32_t v, bool backoff) {
   unsigned ns = 32;
@@ -1103,7 +1106,7 @@ __device__ __forceinline__ void wait_above(const uint32_t* p, uint32_t v, bool b
     SB_WD_CHECK("wait_above", v, ld_acquire(p));
     if (backoff) {
       __nanosleep(ns);
-      ns = ns < 256 ? 2 * ns : ns;
+      ns = ns < SB_WA_MAXNS ? 2 * ns : ns;
     }
   }
   sb_perturb();
@@ -1700,7 +1703,7 @@ constexpr int FRING = 32;  // max ring slots (512 TMEM columns / HB)
 //    bands of slack ahead of the output groups).  The host classifies every trail window as ring or copy
 //    (tl.deepmask) and falls back to cols_kernel when a window would straddle.
 #ifndef SB_CG
-#define SB_CG 3
+#define SB_CG 2
 #endif
 constexpr int CG = SB_CG;                      // output warp groups
 constexpr int C2THREADS = 32 * 4 * (1 + CG);   // loader group + CG output groups
