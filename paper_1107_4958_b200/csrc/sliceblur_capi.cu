@@ -316,6 +316,9 @@ constexpr size_t kCols2Smem = (size_t)SB_COLS2_SMEM_KB * 1024;
 #ifndef SB_STREAM_MC
 #define SB_STREAM_MC 1
 #endif
+#ifndef SB_COLS2_SPLIT
+#define SB_COLS2_SPLIT 1
+#endif
 #ifndef SB_COLS2_MINPF
 #define SB_COLS2_MINPF 2
 #endif
@@ -1022,7 +1025,11 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     sb::Tiling ct = make_tiling(sb::Mode::ColsFromMid, plan.pmax, channels, 4, false), pt;
     alignas(64) CUtensorMap mmap;
     if (make_plane_map(mid, g, channels, &mmap) && cols_prefix_tiling(ct, radii, k, plan.pmax, &pt)) {
-      const void* f3 = sb::sweep_ptr_cols2(k);
+      // ring-only tilings with an even number (>= 4) of TMA slots take the split loader (two loader
+      // warps per lane quadrant; C4 1.028 -> 1.002 ms).  With band copies the copies serialise the
+      // two halves and the tiling loses slack to the extra slots (C5 4.14 -> 4.33 ms): one half.
+      const bool split = SB_COLS2_SPLIT && pt.ds == 0 && pt.pf >= 4 && pt.pf % 2 == 0;
+      const void* f3 = split ? sb::sweep_ptr_cols2s(k) : sb::sweep_ptr_cols2(k);
       Launch L3;
       rc = plan_launch(f3, sb::Mode::ColsPrefix, pt, plan.pmax, g.W, total_rows, channels, &L3);
       if (rc) return rc;
@@ -1032,7 +1039,8 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
       void* args[] = {(void*)&mid, (void*)&dst, (void*)&g2, (void*)&plan.taps, (void*)&L3.tl, (void*)&omap,
                       (void*)&mmap};
       // channels are folded into grid.x (fastest varying), as in cols_kernel
-      cudaError_t e = cudaLaunchKernel(f3, dim3(L3.grid.x * L3.grid.y), dim3(sb::C2THREADS), args, L3.smem, st);
+      cudaError_t e = cudaLaunchKernel(f3, dim3(L3.grid.x * L3.grid.y), dim3(split ? sb::C2STHREADS : sb::C2THREADS), args,
+                                       L3.smem, st);
       if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
       return SB_OK;
     }

@@ -1793,8 +1793,16 @@ constexpr int TOBUF = SB_TOBUF;  // output boxes per output warp (double or sing
 constexpr int TRSW = WS + 4;
 constexpr int TDONE = 32;  // output-band done barriers
 
-template <int K>
-__global__ void __launch_bounds__(C2THREADS, 1)
+// SPLIT: eight loader warps.  Warps q and q + 4 share lane quadrant q and alternate band pairs
+// (pair G goes to half G & 1): each waits for its plane bands, forms the pair's prefix from zero
+// and only then takes the running column prefix from the other half (one shared-memory word per
+// column, monotonic per-quadrant counters), so the waits, shared-memory loads and scans of
+// consecutive pairs overlap.  Ring releases stay in band order (pair_done), and with band
+// copies a pair is appended only after the previous pair's copies are out of the ring.
+constexpr int C2STHREADS = C2THREADS + 32 * 4;
+
+template <int K, bool SPLIT = false>
+__global__ void __launch_bounds__(SPLIT ? C2STHREADS : C2THREADS, 1)
     cols2_kernel(const int* __restrict__ mid_in, float* __restrict__ dst, Geometry g, Taps t, Tiling tl,
                  const __grid_constant__ CUtensorMap omap, const __grid_constant__ CUtensorMap mmap) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1805,6 +1813,11 @@ __global__ void __launch_bounds__(C2THREADS, 1)
   // quadrant waits only for the three output warps that read its TMEM lanes: one ld.acquire per
   // output band instead of an mbarrier all four quadrants arrive on.
   __shared__ uint32_t out_cnt[4][CG];
+  // SPLIT hand-offs per lane quadrant: pairs whose end-of-pair column prefix is published,
+  // pairs released to the output groups (with their band copies made), and the prefixes
+  __shared__ uint32_t lcarry_cnt[4], pair_done[4];
+  __shared__ int lcarry_s[2][WS];
+  constexpr int NLW = SPLIT ? 8 : 4;  // loader warps
   const int ch = blockIdx.x % g.in_px;
   const int sidx = blockIdx.x / g.in_px;
   const int strip = sidx % tl.nstrips;
@@ -1826,6 +1839,7 @@ __global__ void __launch_bounds__(C2THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) ring_cnt[i] = 0;
     for (int i = 0; i < 4 * CG; ++i) (&out_cnt[0][0])[i] = 0;
+    for (int i = 0; i < 4; ++i) lcarry_cnt[i] = pair_done[i] = 0;
     for (int i = 0; i < PF; ++i) {
       mbar_init(&lfull[i], 1);   // the issuing thread's expect_tx + the TMA bytes
       mbar_init(&lempty[i], 4);  // one arrive per loader warp
@@ -1837,7 +1851,168 @@ __global__ void __launch_bounds__(C2THREADS, 1)
   tmem_fence_after();
   const uint32_t tlane = tmem_base_s + ((uint32_t)q << 21);
 
-  if (warp < 4) {
+  if (SPLIT && warp < NLW) {
+    // ------------------------------------------------ loader, two halves alternating pairs
+    const int h = warp >> 2;
+    SegIter sc, so;  // ring bands / the output bands whose completion gates the ring
+    sc.init(T0, T1, wh, g.oy0, t.pmax);
+    so.init(T0, T1, wh, g.oy0, t.pmax);
+    uint32_t v = 0;  // global ring band of the next pair's first band
+    uint32_t G = 0;  // global pair index: pair G is staged in TMA slot G % PF, use G / PF
+    int og = 0, oob = 0;
+    uint32_t ocnt = 0;
+    int slot = 0;                           // v % NB
+    int cslot = tl.copy_e % NB, dslot = 0;  // as in the one-half loader (every warp tracks them)
+    const int dist = PF - 2;                // a half issues its pairs dist pairs ahead (PF even, >= 4)
+    for (; sc.valid; sc.next()) {
+      const int* mcol = mid_in + ch * g.mid_ch + (long long)sc.img * g.mid_img + xc;
+      const long long mrow = g.mid_row;
+      const int vstart = sc.a - 1 - t.pmax;
+      const int zc = ch * g.nimg + sc.img;
+      const int npairs = (sc.nbands + 1) / 2;
+      const uint32_t G0 = G;
+      // pair pp of this segment, by lane 0 of the q = 0 warp of the half that owns it
+      auto issue = [&](int pp) {
+        if (q == 0 && lane == 0 && pp < npairs) {
+          const uint32_t Gi = G0 + (uint32_t)pp;
+          const int is = (int)(Gi % (uint32_t)PF);
+          mbar_wait(&lempty[is], ((Gi / (uint32_t)PF) & 1) ^ 1);
+          mbar_expect_tx(&lfull[is], 2 * HB * WS * 4);
+          tma_load_3d(lring + is * (2 * HB * WS), &mmap, x0, vstart + pp * 2 * HB, zc, &lfull[is]);
+        }
+      };
+      for (int pp = 0; pp < dist && pp < npairs; ++pp)
+        if (((G0 + (uint32_t)pp) & 1u) == (uint32_t)h) issue(pp);
+      for (int pp = 0; pp < npairs; ++pp, ++G) {
+        const int nbp = min(2, sc.nbands - 2 * pp);  // bands in this pair
+        bool cp[2] = {false, false};
+        if (DS > 0) {
+#pragma unroll
+          for (int d = 0; d < 2; ++d) cp[d] = d < nbp && (long long)v + d >= (long long)NB - tl.copy_e;
+        }
+        if ((G & 1u) == (uint32_t)h) {
+          issue(pp + dist);
+          // every output band reading ring bands v+d - NB from TMEM is done
+          while (so.valid && (long long)(so.gb0 + (uint32_t)oob) + tl.lag <= (long long)v + nbp - 1) {
+            wait_above(&out_cnt[q][og], ocnt, false);
+            if (++og == CG) {
+              og = 0;
+              ++ocnt;
+            }
+            if (++oob == (so.b - so.a + HB - 1) / HB) {
+              so.next();
+              oob = 0;
+            }
+          }
+          tmem_fence_after();
+          const int ls = (int)(G % (uint32_t)PF);
+          uint32_t cv[2][HB];
+          mbar_wait(&lfull[ls], (G / (uint32_t)PF) & 1);
+          int cprefix = 0;  // prefix within the pair; the carry of the earlier pairs is added below
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            if (d >= nbp) break;
+            const int v0 = vstart + (2 * pp + d) * HB;
+            if (v0 >= 0 && v0 + HB <= g.H) {
+              const int* lp = lring + ls * (2 * HB * WS) + d * (HB * WS) + c;
+              int e[HB];
+#pragma unroll
+              for (int r = 0; r < HB; ++r) e[r] = lp[r * WS];
+              int odd = cprefix;
+#pragma unroll
+              for (int r = 0; r < HB; r += 2) {
+                cv[d][r] = (uint32_t)(odd + e[r]);
+                odd = odd + e[r] + e[r + 1];
+                cv[d][r + 1] = (uint32_t)odd;
+              }
+              cprefix = odd;
+            } else {
+              // rows beyond the image edges replicate the border row (filtering.py:10-13)
+#pragma unroll
+              for (int r = 0; r < HB; ++r) {
+                cprefix += __ldg(mcol + (long long)min(max(v0 + r, 0), g.H - 1) * mrow);
+                cv[d][r] = (uint32_t)cprefix;
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&lempty[ls]);
+          // the running prefix at the end of pair G - 1 (0 at a segment start); waiting also keeps
+          // lcarry_cnt monotonic
+          if (G > 0) wait_above(&lcarry_cnt[q], G - 1, false);
+          const int carry = pp > 0 ? lcarry_s[h ^ 1][c] : 0;
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            if (d >= nbp) break;
+#pragma unroll
+            for (int r = 0; r < HB; ++r) cv[d][r] += (uint32_t)carry;
+          }
+          lcarry_s[h][c] = carry + cprefix;
+          __syncwarp();
+          if (lane == 0) st_release(&lcarry_cnt[q], G + 1);
+          // with band copies, pair G - 1's copies leave the ring before this pair overwrites bands
+          if (DS > 0 && G > 0) wait_above(&pair_done[q], G - 1, false);
+          {
+            int sl = slot;
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+              if (d >= nbp) break;
+              tmem_st16(tlane + (uint32_t)(sl * HB), cv[d]);
+              if (sl == 0) tmem_st16(tlane + (uint32_t)D, cv[d]);  // mirror: lag windows never wrap
+              if (++sl == NB) sl = 0;
+            }
+          }
+          tmem_wait_st();
+          tmem_fence_before();
+          __syncwarp();
+          // releases in band order
+          if (DS == 0 && G > 0) wait_above(&pair_done[q], G - 1, false);
+          if (lane == 0) st_release(&ring_cnt[q], v + (uint32_t)nbp);
+          if (DS > 0) {
+            uint32_t old[2][HB];
+            int cs = cslot;
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+              if (d >= nbp) break;
+              if (cp[d]) tmem_ld16(tlane + (uint32_t)(cs * HB), old[d]);
+              if (++cs == NB) cs = 0;
+            }
+            tmem_wait_ld();
+            int ds2 = dslot;
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+              if (d >= nbp) break;
+              if (cp[d]) {
+                int* dp = dring + ds2 * (HB * WS) + c;
+#pragma unroll
+                for (int r = 0; r < HB; ++r) dp[r * WS] = (int)old[d][r];
+                if (ds2 == 0) {  // mirror of copy slot 0 after the last slot: trail windows never wrap
+                  int* mp = dring + DS * (HB * WS) + c;
+#pragma unroll
+                  for (int r = 0; r < HB; ++r) mp[r * WS] = (int)old[d][r];
+                }
+                if (++ds2 == DS) ds2 = 0;
+              }
+            }
+            tmem_fence_before();
+            __syncwarp();
+          }
+          if (lane == 0) st_release(&pair_done[q], G + 1);
+        }
+        // ring / copy positions after this pair (every loader warp, also for the other half's pairs)
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          if (d >= nbp) break;
+          if (++slot == NB) slot = 0;
+          if (DS > 0) {
+            if (cp[d] && ++dslot == DS) dslot = 0;
+            if (++cslot == NB) cslot = 0;
+          }
+        }
+        v += (uint32_t)nbp;
+      }
+    }
+  } else if (!SPLIT && warp < 4) {
     // ------------------------------------------------ loader
     SegIter sc, so;  // ring bands / the output bands whose completion gates the ring
     sc.init(T0, T1, wh, g.oy0, t.pmax);
@@ -1973,8 +2148,8 @@ __global__ void __launch_bounds__(C2THREADS, 1)
     }
   } else {
     // ------------------------------------------------ output groups
-    const int grp = warp / 4 - 1;
-    const int ow = warp - 4;  // output warp 0 .. 4*CG-1 (staging buffers)
+    const int grp = (warp - NLW) / 4;
+    const int ow = warp - NLW;  // output warp 0 .. 4*CG-1 (staging buffers)
     uint32_t onum = 0;
     int obsel = 0;
     SegIter so;
@@ -2571,6 +2746,7 @@ int launch_cols_generic(void* mid, float* dst, const Geometry& g, const TapsG& t
                         cudaStream_t st);
 const void* sweep_ptr_cols(int k);   // ColsFromMid (source type unused)
 const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
+const void* sweep_ptr_cols2s(int k); // ColsFromMid, prefix form, split loader (eight loader warps)
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)
 const void* sweep_ptr_stream_mc(int k);   // streaming row pass, interleaved float32 channels staged once
 const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
@@ -2627,6 +2803,13 @@ const void* cols2_ptr_for(int k) {
 #define SB_COLS2(KK) cols2_kernel<KK>
   SB_K_CASES(SB_COLS2)
 #undef SB_COLS2
+}
+
+template <typename Unused = void>
+const void* cols2s_ptr_for(int k) {
+#define SB_COLS2S(KK) cols2_kernel<KK, true>
+  SB_K_CASES(SB_COLS2S)
+#undef SB_COLS2S
 #undef SB_K_CASES
 }
 
