@@ -468,6 +468,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     e_ms = D.max_over_ranks((time.perf_counter() - t0) * 1e3, device=device)
     e_value = px_total * e_steps / (e_ms / 1e3) / 1e6
+    link = _host_link_gbs(torch, device) if rank == 0 else None
 
     # sampled parity on this rank's output (not timed)
     from oracle import oracle
@@ -542,7 +543,10 @@ def run_ours(args, cfg):
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                      "algorithmic_bytes_per_step": alg_bytes, "kernels_per_step": kinds},
         "e2e": {"value": round(e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(in_bytes),
-                "d2h_bytes_per_step": int(out_bytes), "api": e2e_api},
+                "d2h_bytes_per_step": int(out_bytes), "api": e2e_api,
+                # this box's pinned-copy rates (256 MiB, after the e2e loop): the float32 result is
+                # 4 B/px of D2H, so e2e <= d2h_gbs / 4 Gpx/s whatever the kernel does
+                "host_link_gbs": link},
         "gpu_launches": int(args.steps * n_launch) if n_launch is not None else None,
         "parity": {"max_abs": max_abs, "rmse": rmse, "scope": "rank-0 image 0 vs C oracle"},
         "quality": quality,
@@ -553,6 +557,26 @@ def run_ours(args, cfg):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _host_link_gbs(torch, device, nbytes: int = 256 << 20):
+    """Pinned host <-> device copy rates of this box (GB/s), to read the e2e number against."""
+    try:
+        dbuf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        hbuf = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        res = {}
+        for name, fn in (("h2d", lambda: dbuf.copy_(hbuf, non_blocking=True)),
+                         ("d2h", lambda: hbuf.copy_(dbuf, non_blocking=True))):
+            fn()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            res[name] = round(3 * nbytes / (time.perf_counter() - t0) / 1e9, 1)
+        return res
+    except Exception:  # measurement aid only
+        return None
 
 
 def launch_check():

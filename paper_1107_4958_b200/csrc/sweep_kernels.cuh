@@ -20,11 +20,17 @@
 //                       bands of a 128-column strip into shared memory, consumer warps form the
 //                       row values, the TMEM column ring and the outputs (uint8: biased-fp32
 //                       prefixes, IDP4A scans, FADD2/FFMA2 on row pairs, two bands per turn)
+//                       (opt-in variants: three CTAs per SM, one band per turn, paired consumer
+//                       warps - two warps per TMEM lane quadrant alternating bands)
 //   stream_rows_kernel  two-launch row pass (float32): full-width 16-row bands streamed in
-//                       128-column chunks with the row prefix carried in a ring -> int32 plane
+//                       128-column chunks (four staged chunks in flight per producer warp) with
+//                       the row prefix carried in a ring -> int32 plane
+//   stream_rows_mc_kernel  the same for 2..4 interleaved channels: bands of virtual (row,
+//                       channel) rows, the band's image rows staged once by bulk copies
 //   cols2_kernel        two-launch column pass: TMA loads of plane bands, loader warps append
-//                       the column prefix to the TMEM ring, output groups read windows; trails
-//                       older than the ring come from shared-memory band copies
+//                       the column prefix to the TMEM ring, two output groups read windows;
+//                       trails older than the ring come from shared-memory band copies;
+//                       ring-only tilings use the split loader (two loader warps per quadrant)
 //   cols_kernel         running-sum column pass (fallback when no tensor map fits)
 //   rows_kernel         tiled row pass (other source types, row pass alone)
 // and, in their own translation units: sweep_wide.cu (fusedw_kernel, one-launch float32 for
