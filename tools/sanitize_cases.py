@@ -43,6 +43,13 @@ CASES = [
     ("f32 wide fused, batch, odd width", nat.SB_PATH_FUSED_WIDE, np.float32, (3, 400, 517), 4, 40.0),
     ("u8 row-tile", nat.SB_PATH_U8_ROWTILE, np.uint8, (9, 300, 1000), 3, 10.0),
     ("u8 row-tile, tiny images", nat.SB_PATH_U8_ROWTILE, np.uint8, (61, 37, 150), 3, 3.0),
+    # kernels of the last round-2 sessions
+    ("u8 paired consumer warps", nat.SB_PATH_U8_PAIRED, np.uint8, (5, 37, 150), 3, 3.0),
+    ("u8 paired consumer warps, odd 61 images", nat.SB_PATH_U8_PAIRED, np.uint8, (61, 37, 150), 3, 3.0),
+    ("u8 paired consumer warps, 1000 wide", nat.SB_PATH_U8_PAIRED, np.uint8, (9, 300, 1000), 3, 10.0),
+    ("f32 stream rows + cols2 split loader (ring only)", nat.SB_PATH_AUTO, np.float32, (1, 500, 600), 4, 40.0),
+    ("f32 3 channels: stream_rows_mc + cols2 split loader", nat.SB_PATH_AUTO, np.float32, (2, 300, 388, 3), 4, 40.0),
+    ("f32 4 channels, short images: stream_rows_mc", nat.SB_PATH_UNFUSED, np.float32, (5, 13, 388, 4), 3, 5.0),
 ]
 
 
