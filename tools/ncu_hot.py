@@ -1,6 +1,9 @@
 """Hot SASS regions of one kernel in an ncu report: runs of equal execution count.
 
-    python tools/ncu_hot.py REP.ncu-rep [min_frac]
+    python tools/ncu_hot.py REP.ncu-rep [min_frac] [KERNEL_REGEX]
+
+Without KERNEL_REGEX the rows of every kernel in the report are merged (addresses restart per
+kernel); give one (e.g. cols2, stream_rows) for a report that holds several kernels.
 """
 import csv
 import io
@@ -9,7 +12,8 @@ import sys
 
 rep = sys.argv[1]
 minf = float(sys.argv[2]) if len(sys.argv) > 2 else 0.004
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+kfilter = ["-k", f"regex:{sys.argv[3]}"] if len(sys.argv) > 3 else []
+txt = subprocess.run(["ncu", "-i", rep, *kfilter, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 h = rows[1]
