@@ -316,6 +316,9 @@ constexpr size_t kCols2Smem = (size_t)SB_COLS2_SMEM_KB * 1024;
 #ifndef SB_STREAM_MC
 #define SB_STREAM_MC 1
 #endif
+#ifndef SB_STREAM_ALL_TYPES
+#define SB_STREAM_ALL_TYPES 1
+#endif
 #ifndef SB_COLS2_SPLIT
 #define SB_COLS2_SPLIT 1
 #endif
@@ -693,10 +696,13 @@ bool needs_wide(int pmax) { return 2LL * pmax + 1 > sb::kWideSpan; }
 
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
-bool stream_rows_fits(int src_dtype, int pmax) {
+// The streaming row pass takes float32 sources with any channel count and one-channel sources
+// of every other type (float64 is the reference's own dtype: 8192^2 sigma 64 went from 2.26 to
+// 0.43 ms with it; interleaved non-float32 channels keep the tiled row pass).
+bool stream_rows_fits(int src_dtype, int pmax, int channels) {
   const int xs = -(((pmax + 1) + 15) & ~15);
   const int lagc = (sb::CW - 1 - xs + pmax) / sb::CW;
-  return src_dtype == SB_DTYPE_F32 && lagc + 1 < sb::NSLOT;
+  return (src_dtype == SB_DTYPE_F32 || (SB_STREAM_ALL_TYPES && channels == 1)) && lagc + 1 < sb::NSLOT;
 }
 
 bool tiled_rows_fits(sb::Mode m, int pmax, int channels, int es) {
@@ -723,7 +729,13 @@ Route route_2d(int src_dtype, int64_t width, int channels, const int64_t* radii,
     r.cols = ColPath::None;
     return r;
   }
-  if (fast && g_policy != SB_PATH_UNFUSED && fused_fits(pmax, channels, es)) {
+  // One-channel uint8 past the packed (float2-prefix) tiling: the unpacked fused sweep is slower
+  // than the streaming row pass + cols2 (4096^2 p_max 77: 0.189 vs 0.114 ms; 8192^2 p_max 103:
+  // 0.652 vs 0.321 ms), so AUTO takes two launches there.
+  const bool u8_unpacked = SB_STREAM_ALL_TYPES && src_dtype == SB_DTYPE_U8 && channels == 1 &&
+                           !make_tiling(sb::Mode::Fused, pmax, 1, 1, true).packed &&
+                           stream_rows_fits(src_dtype, pmax, channels);
+  if (fast && g_policy != SB_PATH_UNFUSED && fused_fits(pmax, channels, es) && !u8_unpacked) {
     r.rows = RowPath::Fused;
     r.cols = ColPath::None;
     return r;
@@ -736,7 +748,7 @@ Route route_2d(int src_dtype, int64_t width, int channels, const int64_t* radii,
     return r;
   }
   if (fast) {
-    if (stream_rows_fits(src_dtype, pmax))
+    if (stream_rows_fits(src_dtype, pmax, channels))
       r.rows = RowPath::Stream;
     else if (tiled_rows_fits(sb::Mode::RowsToMid, pmax, channels, es))
       r.rows = RowPath::Tiled;
@@ -981,9 +993,13 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     // image rows staged once for all channels (stream_rows_mc_kernel); else one channel per CTA
     const bool mc = SB_STREAM_MC && channels >= 2 && channels <= 4 && g.in_px == channels && g.aligned16 &&
                     (width * channels) % 4 == 0 && all_rows * width * channels < (1LL << 31);
-    const void* fs = mc ? sb::sweep_ptr_stream_mc(k) : sb::sweep_ptr_stream_f32(k);
+    const void* fs = mc                            ? sb::sweep_ptr_stream_mc(k)
+                     : src_dtype == SB_DTYPE_F32   ? sb::sweep_ptr_stream_f32(k)
+                     : src_dtype == SB_DTYPE_F64   ? sb::sweep_ptr_stream_f64(k)
+                     : src_dtype == SB_DTYPE_U16   ? sb::sweep_ptr_stream_u16(k)
+                                                   : sb::sweep_ptr_stream_u8(k);
     const size_t stage = mc ? (size_t)sb::STG * sb::mc_rows(channels) * (sb::CW * channels * sizeof(float) + sb::SRB_PAD)
-                            : (size_t)sb::NPROD * sb::STG * 8 * (sb::CW * sizeof(float) + sb::SRB_PAD);
+                            : (size_t)sb::NPROD * sb::stream_stages(g.es) * 8 * (sb::CW * (size_t)g.es + sb::SRB_PAD);
     const size_t smem = stage + (size_t)sb::HB * sb::RLS * sizeof(int);
     FnFacts ff;
     DevFacts df;

@@ -2289,6 +2289,8 @@ constexpr int SRB_PAD = 16;     // staged rows are CW*4 + 16 bytes apart: 16 (mo
 #define SB_STREAM_STAGES 4
 #endif
 constexpr int STG = SB_STREAM_STAGES;
+// float64 sources stage 8-byte elements: two chunks keep the CTA below half an SM's shared memory
+constexpr int stream_stages(size_t es) { return es == 8 ? 2 : STG; }
 // consumer warps: SRG row groups of CW threads; group rg forms rows [rg * HB / SRG, (rg + 1) * HB / SRG)
 // of each output chunk.  Two groups (8 rows per thread, 20 warps per SM instead of 12) measured
 // 3.7 % slower on C5 (4.416 vs 4.257 ms): the per-thread address work doubles.  Default 1.
@@ -2306,6 +2308,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
                        int nbands_total, int* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
+  constexpr int STG = stream_stages(sizeof(Tin));  // staged chunks per producer warp (float64: two CTAs per SM)
   const int warp = threadIdx.x >> 5;
   const bool producer = warp >= SCONS;
   const int qtotal = g.W - xs + t.pmax;  // virtual columns q = x - xs, x in [xs, W + pmax)
@@ -2344,16 +2347,18 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
         const int img = (int)(trow / g.H), v = (int)(trow - (long long)img * g.H);
         rowp[rr] = src + (long long)img * g.in_img + (long long)v * g.in_row + ch;
       }
-      const bool vec = g.aligned16 && g.in_px == 1 && sizeof(Tin) == 4;
+      const bool vec = g.aligned16 && g.in_px == 1;
       auto issue = [&](int j, int buf) {
         const int xq0 = xs + j * CW;  // 16-aligned first column of chunk j
         if (vec && xq0 >= 0 && xq0 + CW <= g.W) {
-          // interior chunk: 16-byte copies, 8 rows x CW/4 vectors
+          // interior chunk: 16-byte copies, 8 rows x VPR vectors (xq0 is a multiple of 16 columns)
+          constexpr int VPR = CW * (int)sizeof(Tin) / 16;
 #pragma unroll
-          for (int it = 0; it < 8 * CW / 4 / 32; ++it) {
+          for (int it = 0; it < 8 * VPR / 32; ++it) {
             const int idx = lane + 32 * it;
-            const int rr = idx / (CW / 4), e4 = idx - rr * (CW / 4);
-            cp_async16(mystage + (buf * 8 + rr) * rowbytes + 16 * e4, rowp[rr] + xq0 + 4 * e4);
+            const int rr = idx / VPR, e4 = idx - rr * VPR;
+            cp_async16(mystage + (buf * 8 + rr) * rowbytes + 16 * e4,
+                       (const unsigned char*)(rowp[rr] + xq0) + 16 * e4);
           }
         } else {
 #pragma unroll
@@ -2403,12 +2408,20 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
           const int rr = lane & 7, sc = (lane >> 3) + 4 * pass;
-          const Tin* e = (const Tin*)(cur + rr * rowbytes) + sc * CH;
+          // the lane's CH elements by 16-byte shared-memory loads (staged rows and sub-chunks are
+          // 16-byte aligned for every element size)
+          union {
+            uint4 q[CH * sizeof(Tin) / 16];
+            Tin e[CH];
+          } u;
+          const uint4* ep = (const uint4*)(cur + rr * rowbytes + sc * CH * (int)sizeof(Tin));
+#pragma unroll
+          for (int m = 0; m < (int)(CH * sizeof(Tin) / 16); ++m) u.q[m] = ep[m];
           int v[CH];
           int tot = 0;
 #pragma unroll
           for (int m = 0; m < CH; ++m) {
-            tot += to_fixed<Tin>(e[m], t, bad);
+            tot += to_fixed<Tin>(u.e[m], t, bad);
             v[m] = tot;
           }
           // inclusive scan of the chunk totals over the row's 4 lanes (rr, rr+8, rr+16, rr+24)
@@ -2716,9 +2729,9 @@ const void* stream_mc_ptr_for(int k) {
   }
 }
 
-template <typename Unused = void>  // a template: instantiates its kernels only where it is called
-const void* stream_ptr_for_f32(int k) {
-#define SB_STREAM(KK) stream_rows_kernel<float, KK>
+template <typename Tin>  // a template: instantiates its kernels only where it is called
+const void* stream_ptr_for(int k) {
+#define SB_STREAM(KK) stream_rows_kernel<Tin, KK>
   switch (k) {
     case 1: return (const void*)SB_STREAM(1);
     case 2: return (const void*)SB_STREAM(2);
@@ -2754,6 +2767,9 @@ const void* sweep_ptr_cols(int k);   // ColsFromMid (source type unused)
 const void* sweep_ptr_cols2(int k);  // ColsFromMid, prefix form
 const void* sweep_ptr_cols2s(int k); // ColsFromMid, prefix form, split loader (eight loader warps)
 const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources)
+const void* sweep_ptr_stream_f64(int k);  // streaming row pass, one-channel float64 / uint8 / uint16 sources
+const void* sweep_ptr_stream_u8(int k);
+const void* sweep_ptr_stream_u16(int k);
 const void* sweep_ptr_stream_mc(int k);   // streaming row pass, interleaved float32 channels staged once
 const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
 const void* sweep_ptr_fused5(int k);      // fused sweep, two bands per consumer iteration (uint8, one channel)

@@ -262,3 +262,30 @@ def test_interleaved_channels_streaming_rows(shape, k, sigma):
         for c in range(shape[3]):
             ref = O.separable_filter_2d(np.ascontiguousarray(x[n, :, :, c]), kern.radii, kern.weights)
             assert float(np.abs(got[n, :, :, c] - ref).max()) <= BAR
+
+
+# The streaming row pass on one-channel uint8 / uint16 / float64 sources (radii past the packed
+# fused sweep): 16-byte staged rows for every element size, and the element path for rows that
+# are not 16-byte multiples.
+@pytest.mark.parametrize("dtype,shape,k,sigma", [
+    (np.uint8, (2, 300, 512), 4, 30.0),
+    (np.uint8, (1, 200, 333), 4, 20.0),     # unaligned rows: element staging
+    (np.uint16, (1, 400, 528), 4, 40.0),
+    (np.float64, (1, 300, 416), 5, 60.0),
+    (np.float64, (3, 130, 275), 3, 25.0),   # unaligned rows, several images
+], ids=["u8", "u8-unaligned", "u16", "f64", "f64-unaligned-batch"])
+def test_streaming_rows_every_source_type(dtype, shape, k, sigma):
+    rng = np.random.default_rng(shape[1] + shape[2])
+    scale = 65535 if dtype == np.uint16 else 255
+    x = (rng.random(shape) * scale).astype(dtype)
+    kern = A.table_kernel(k, sigma)
+    assert 31 < kern.max_radius < min(shape[1], shape[2])
+    bound = None if dtype in (np.uint8, np.uint16) else float(scale)
+    xt = torch.from_numpy(x).cuda()
+    got = F.separable_filter_batch(xt, kern, value_bound=bound).cpu().numpy()
+    with nat.path_policy(nat.SB_PATH_GENERIC):
+        gen = F.separable_filter_batch(xt, kern, value_bound=bound).cpu().numpy()
+    np.testing.assert_array_equal(got, gen)
+    for n in range(shape[0]):
+        ref = O.separable_filter_2d(x[n], kern.radii, kern.weights)
+        assert float(np.abs(got[n] - ref).max()) * 255.0 / scale <= BAR

@@ -156,7 +156,7 @@ def test_one_launch_routing_per_policy(lib):
     same route as the launch).  AUTO: float32 one launch up to p_max 31 (fused_kernel), two
     launches past it; SB_PATH_FUSED_WIDE extends the one-launch range to every float32 radius
     the wide sweep's tiling admits (p_max <= 279 for k = 1, C5's 257 included) and leaves interleaved channels and
-    float64 on the two-launch path; SB_PATH_U8_ROWTILE keeps uint8 at one launch."""
+    float64 on the two-launch path; SB_PATH_U8_ROWTILE keeps small-radius uint8 at one launch."""
 
     def ws(dtype, p, ch=1):
         r = (ctypes.c_int64 * 1)(p)
@@ -171,6 +171,10 @@ def test_one_launch_routing_per_policy(lib):
         assert ws(nat.SB_DTYPE_F64, 100) > 0
     assert ws(nat.SB_DTYPE_F32, 82) > 0                 # the policy is scoped
     with nat.path_policy(nat.SB_PATH_U8_ROWTILE):
-        for p in (0, 7, 23, 100):
+        for p in (0, 7, 23):
             assert ws(nat.SB_DTYPE_U8, p) == 0, p
+    # uint8, one channel: the packed fused sweep up to p_max 31, past it the streaming row pass +
+    # cols2 (faster than the unpacked fused sweep); float64 streams too (one int32 plane)
+    assert ws(nat.SB_DTYPE_U8, 31) == 0 and ws(nat.SB_DTYPE_U8, 32) == 4 * 4096 * 4096
+    assert ws(nat.SB_DTYPE_U8, 100) == 4 * 4096 * 4096 and ws(nat.SB_DTYPE_F64, 100) == 4 * 4096 * 4096
     assert lib.sb_set_path_policy(nat.SB_PATH_U8_TWO_BAND + 1) == -1
