@@ -699,10 +699,13 @@ size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 // The streaming row pass takes float32 sources with any channel count and one-channel sources
 // of every other type (float64 is the reference's own dtype: 8192^2 sigma 64 went from 2.26 to
 // 0.43 ms with it; interleaved non-float32 channels keep the tiled row pass).
-bool stream_rows_fits(int src_dtype, int pmax, int channels) {
+bool stream_rows_fits(int src_dtype, int pmax, int channels, int64_t width) {
   const int xs = -(((pmax + 1) + 15) & ~15);
   const int lagc = (sb::CW - 1 - xs + pmax) / sb::CW;
-  return (src_dtype == SB_DTYPE_F32 || (SB_STREAM_ALL_TYPES && channels == 1)) && lagc + 1 < sb::NSLOT;
+  // interleaved channels of the other types: only rows the bulk copies can stage (16-byte multiples)
+  const bool other = SB_STREAM_ALL_TYPES &&
+                     (channels == 1 || (channels <= 4 && (width * channels * dtype_size(src_dtype)) % 16 == 0));
+  return (src_dtype == SB_DTYPE_F32 || other) && lagc + 1 < sb::NSLOT;
 }
 
 bool tiled_rows_fits(sb::Mode m, int pmax, int channels, int es) {
@@ -734,7 +737,7 @@ Route route_2d(int src_dtype, int64_t width, int channels, const int64_t* radii,
   // 0.652 vs 0.321 ms), so AUTO takes two launches there.
   const bool u8_unpacked = SB_STREAM_ALL_TYPES && src_dtype == SB_DTYPE_U8 && channels == 1 &&
                            !make_tiling(sb::Mode::Fused, pmax, 1, 1, true).packed &&
-                           stream_rows_fits(src_dtype, pmax, channels);
+                           stream_rows_fits(src_dtype, pmax, channels, width);
   if (fast && g_policy != SB_PATH_UNFUSED && fused_fits(pmax, channels, es) && !u8_unpacked) {
     r.rows = RowPath::Fused;
     r.cols = ColPath::None;
@@ -748,7 +751,7 @@ Route route_2d(int src_dtype, int64_t width, int channels, const int64_t* radii,
     return r;
   }
   if (fast) {
-    if (stream_rows_fits(src_dtype, pmax, channels))
+    if (stream_rows_fits(src_dtype, pmax, channels, width))
       r.rows = RowPath::Stream;
     else if (tiled_rows_fits(sb::Mode::RowsToMid, pmax, channels, es))
       r.rows = RowPath::Tiled;
@@ -992,13 +995,15 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     // interleaved channels with 16-byte aligned rows: bands of virtual (row, channel) rows, the
     // image rows staged once for all channels (stream_rows_mc_kernel); else one channel per CTA
     const bool mc = SB_STREAM_MC && channels >= 2 && channels <= 4 && g.in_px == channels && g.aligned16 &&
-                    (width * channels) % 4 == 0 && all_rows * width * channels < (1LL << 31);
-    const void* fs = mc                            ? sb::sweep_ptr_stream_mc(k)
+                    (width * channels * g.es) % 16 == 0 && all_rows * width * channels < (1LL << 31) &&
+                    (src_dtype == SB_DTYPE_F32 || SB_STREAM_ALL_TYPES);
+    const void* fs = mc                            ? sb::sweep_ptr_stream_mc(src_dtype, k)
                      : src_dtype == SB_DTYPE_F32   ? sb::sweep_ptr_stream_f32(k)
                      : src_dtype == SB_DTYPE_F64   ? sb::sweep_ptr_stream_f64(k)
                      : src_dtype == SB_DTYPE_U16   ? sb::sweep_ptr_stream_u16(k)
                                                    : sb::sweep_ptr_stream_u8(k);
-    const size_t stage = mc ? (size_t)sb::STG * sb::mc_rows(channels) * (sb::CW * channels * sizeof(float) + sb::SRB_PAD)
+    const size_t stage = mc ? (size_t)sb::stream_stages(g.es) * sb::mc_rows(channels) *
+                                  (sb::CW * channels * (size_t)g.es + sb::SRB_PAD)
                             : (size_t)sb::NPROD * sb::stream_stages(g.es) * 8 * (sb::CW * (size_t)g.es + sb::SRB_PAD);
     const size_t smem = stage + (size_t)sb::HB * sb::RLS * sizeof(int);
     FnFacts ff;

@@ -2518,7 +2518,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
 }
 
 // ---------------------------------------------------------------- streaming row pass, interleaved channels
-// float32 sources with C = 2..4 interleaved channels and 16-byte aligned rows (C4).  The band
+// Sources with C = 2..4 interleaved channels and 16-byte aligned rows (C4; any element type).  The band
 // is HB VIRTUAL rows vr = t * C + ch (tall row t, channel ch), so a band touches at most
 // HB / C + 2 image rows.  The two producer warps stage those rows ONCE per chunk, interleaved
 // as they lie in memory (16-byte cp.async; the per-element 4-byte gather of
@@ -2528,15 +2528,17 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
 // [channel][tall row][W], dense, below 2^31 elements (32-bit store offsets).
 constexpr int mc_rows(int C) { return (HB + C - 1) / C + 1; }
 
-template <int K>
+template <typename Tin, int K>
 __global__ void __launch_bounds__(STREAM_THREADS, 2)
-    stream_rows_mc_kernel(const float* __restrict__ src, int* __restrict__ mid_out, Geometry g, Taps t, int xs,
+    stream_rows_mc_kernel(const Tin* __restrict__ src, int* __restrict__ mid_out, Geometry g, Taps t, int xs,
                           int nbands_total, int* status) {
   static_assert(SRG == 1, "the interleaved streaming row pass assumes one consumer row group");
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
+  constexpr int STG = stream_stages(sizeof(Tin));
+  constexpr int ES = (int)sizeof(Tin);
   __shared__ __align__(8) uint64_t sfull[STG];  // staged chunk landed (bulk-copy bytes / edge-chunk arrive)
-  __shared__ const float* rowp_s[HB / 2 + 2];   // the band's image rows (clamped at the end of the tall image)
+  __shared__ const Tin* rowp_s[HB / 2 + 2];     // the band's image rows (clamped at the end of the tall image)
   const int warp = threadIdx.x >> 5;
   const bool producer = warp >= SCONS;
   const int C = g.in_px;
@@ -2545,7 +2547,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
   const int nout = (g.W + CW - 1) / CW;
   const int lagc = (CW - 1 - xs + t.pmax) / CW;
   const int ntmax = (HB + C - 1) / C + 1;
-  const int srb = CW * C * 4 + SRB_PAD;       // staged image row: CW pixels of C floats (+ 16: odd multiple of 16)
+  const int srb = CW * C * ES + SRB_PAD;      // staged image row: CW pixels of C elements (+ 16 bytes)
   unsigned char* stage = smem;                // [STG][ntmax][srb]
   int* P = (int*)(smem + STG * ntmax * srb);  // [HB][RLS]
   if (threadIdx.x == 0) {
@@ -2589,18 +2591,21 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
         unsigned char* sbuf = stage + buf * ntmax * srb;
         if (interior(j)) {
           if (ptid == 0) {
-            mbar_expect_tx(&sfull[buf], (uint32_t)(nt * CW * C * 4));
+            mbar_expect_tx(&sfull[buf], (uint32_t)(nt * CW * C * ES));
             for (int i = 0; i < nt; ++i)
-              bulk_g2s(sbuf + i * srb, rowp_s[i] + (long long)xq0 * C, (uint32_t)(CW * C * 4), &sfull[buf]);
+              bulk_g2s(sbuf + i * srb, rowp_s[i] + (long long)xq0 * C, (uint32_t)(CW * C * ES), &sfull[buf]);
           }
         } else {
           for (int i = 0; i < nt; ++i) {
-            const float* rp = rowp_s[i];
+            const Tin* rp = rowp_s[i];
             for (int e = ptid; e < CW * C; e += 32 * NPROD) {
               const int px = e / C, cc = e - px * C;
               const int x = min(max(xq0 + px, 0), g.W - 1);
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(sbuf + i * srb + 4 * e)),
-                           "l"(rp + (long long)x * C + cc));
+              if constexpr (ES == 4)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(sbuf + i * srb + 4 * e)),
+                             "l"(rp + (long long)x * C + cc));
+              else
+                *(Tin*)(sbuf + i * srb + ES * e) = rp[(long long)x * C + cc];  // visible after the named barrier
             }
           }
           cp_async_commit();
@@ -2611,7 +2616,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
       const int rr = lane & 7;
       const long long vr = vr0 + min(8 * pw + rr, nrows - 1);
       const long long tt = vr / C;
-      const int lane_off = (int)(tt - t_first) * srb + (int)(vr - tt * C) * 4;
+      const int lane_off = (int)(tt - t_first) * srb + (int)(vr - tt * C) * ES;
       int carry = 0;
       for (int j = 0; j < STG - 1 && j < nin; ++j) issue(j);
       RangeAcc bad;
@@ -2632,12 +2637,12 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
           const int sc = (lane >> 3) + 4 * pass;
-          const float* e = (const float*)cur + sc * CH * C;
+          const Tin* e = (const Tin*)cur + sc * CH * C;
           int v[CH];
           int tot = 0;
 #pragma unroll
           for (int m = 0; m < CH; ++m) {
-            tot += to_fixed<float>(e[m * C], t, bad);
+            tot += to_fixed<Tin>(e[m * C], t, bad);
             v[m] = tot;
           }
           int inc = tot;
@@ -2715,17 +2720,17 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
   }
 }
 
-template <typename Unused = void>
+template <typename Tin>
 const void* stream_mc_ptr_for(int k) {
   switch (k) {
-    case 1: return (const void*)stream_rows_mc_kernel<1>;
-    case 2: return (const void*)stream_rows_mc_kernel<2>;
-    case 3: return (const void*)stream_rows_mc_kernel<3>;
-    case 4: return (const void*)stream_rows_mc_kernel<4>;
-    case 5: return (const void*)stream_rows_mc_kernel<5>;
-    case 6: return (const void*)stream_rows_mc_kernel<6>;
-    case 7: return (const void*)stream_rows_mc_kernel<7>;
-    default: return (const void*)stream_rows_mc_kernel<8>;
+    case 1: return (const void*)stream_rows_mc_kernel<Tin, 1>;
+    case 2: return (const void*)stream_rows_mc_kernel<Tin, 2>;
+    case 3: return (const void*)stream_rows_mc_kernel<Tin, 3>;
+    case 4: return (const void*)stream_rows_mc_kernel<Tin, 4>;
+    case 5: return (const void*)stream_rows_mc_kernel<Tin, 5>;
+    case 6: return (const void*)stream_rows_mc_kernel<Tin, 6>;
+    case 7: return (const void*)stream_rows_mc_kernel<Tin, 7>;
+    default: return (const void*)stream_rows_mc_kernel<Tin, 8>;
   }
 }
 
@@ -2770,7 +2775,7 @@ const void* sweep_ptr_stream_f32(int k);  // streaming row pass (float32 sources
 const void* sweep_ptr_stream_f64(int k);  // streaming row pass, one-channel float64 / uint8 / uint16 sources
 const void* sweep_ptr_stream_u8(int k);
 const void* sweep_ptr_stream_u16(int k);
-const void* sweep_ptr_stream_mc(int k);   // streaming row pass, interleaved float32 channels staged once
+const void* sweep_ptr_stream_mc(int src_dtype, int k);  // streaming row pass, interleaved channels staged once
 const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
 const void* sweep_ptr_fused5(int k);      // fused sweep, two bands per consumer iteration (uint8, one channel)
 const void* sweep_ptr_fusedp(int k);      // fused sweep, paired consumer warps (uint8, one channel)

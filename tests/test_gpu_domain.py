@@ -289,3 +289,32 @@ def test_streaming_rows_every_source_type(dtype, shape, k, sigma):
     for n in range(shape[0]):
         ref = O.separable_filter_2d(x[n], kern.radii, kern.weights)
         assert float(np.abs(got[n] - ref).max()) * 255.0 / scale <= BAR
+
+
+# The interleaved-channel streaming row pass on uint8 / uint16 / float64 sources (RGB uint8 is
+# the common case): rows that are 16-byte multiples are staged by bulk copies for every type.
+@pytest.mark.parametrize("dtype,shape,k,sigma", [
+    (np.uint8, (2, 150, 400, 3), 4, 12.0),    # p_max 30
+    (np.uint8, (1, 300, 512, 4), 5, 64.0),    # p_max 170
+    (np.uint8, (3, 13, 400, 3), 3, 5.0),      # images shorter than a band
+    (np.uint16, (1, 200, 264, 3), 4, 30.0),
+    (np.float64, (1, 333, 274, 3), 4, 40.0),
+    (np.float64, (2, 120, 300, 2), 3, 25.0),
+    (np.uint8, (1, 200, 333, 3), 4, 20.0),    # rows not 16-byte multiples: tiled row pass
+], ids=["u8-rgb", "u8-rgba-large", "u8-rgb-short", "u16-rgb", "f64-rgb", "f64-2ch", "u8-rgb-unaligned"])
+def test_interleaved_channels_every_source_type(dtype, shape, k, sigma):
+    rng = np.random.default_rng(shape[1] * shape[2])
+    scale = 65535 if dtype == np.uint16 else 255
+    x = (rng.random(shape) * scale).astype(dtype)
+    kern = A.table_kernel(k, sigma)
+    assert kern.max_radius < min(shape[1], shape[2])
+    bound = None if dtype in (np.uint8, np.uint16) else float(scale)
+    xt = torch.from_numpy(x).cuda()
+    got = F.separable_filter_batch(xt, kern, channels_last=True, value_bound=bound).cpu().numpy()
+    with nat.path_policy(nat.SB_PATH_GENERIC):
+        gen = F.separable_filter_batch(xt, kern, channels_last=True, value_bound=bound).cpu().numpy()
+    np.testing.assert_array_equal(got, gen)
+    for n in range(shape[0]):
+        for c in range(shape[3]):
+            ref = O.separable_filter_2d(np.ascontiguousarray(x[n, :, :, c]), kern.radii, kern.weights)
+            assert float(np.abs(got[n, :, :, c] - ref).max()) * 255.0 / scale <= BAR
