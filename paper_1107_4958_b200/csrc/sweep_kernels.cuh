@@ -2305,15 +2305,16 @@ constexpr int SHB = HB / SRG;  // rows per consumer thread
 template <typename Tin, int K>
 __global__ void __launch_bounds__(STREAM_THREADS, 2)
     stream_rows_kernel(const Tin* __restrict__ src, int* __restrict__ mid_out, Geometry g, Taps t, int xs,
-                       int nbands_total, int* status) {
+                       int nbands_total, int segw, int* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
   constexpr int STG = stream_stages(sizeof(Tin));  // staged chunks per producer warp (float64: two CTAs per SM)
   const int warp = threadIdx.x >> 5;
   const bool producer = warp >= SCONS;
-  const int qtotal = g.W - xs + t.pmax;  // virtual columns q = x - xs, x in [xs, W + pmax)
-  const int nin = (qtotal + CW - 1) / CW;
-  const int nout = (g.W + CW - 1) / CW;
+  // A unit is (band, column segment): segment s covers columns [s * segw, min(W, (s + 1) * segw))
+  // and restarts the row prefix at its own left halo, so images with few rows still fill the
+  // SMs (segw >= W: one segment, the whole row).
+  const int nseg = (g.W + segw - 1) / segw;
   // output chunk o reads prefix columns of input chunks o .. o + lagc
   const int lagc = (CW - 1 - xs + t.pmax) / CW;
   // staged rows and prefix-ring rows are an odd multiple of 16 bytes apart, so the 8 lanes
@@ -2333,7 +2334,12 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
   const int ch = blockIdx.x % g.in_px;  // channel fastest (see cols_kernel)
   uint32_t cin_ctr = 0, out_ctr = 0;    // input chunks / output chunks completed by this CTA
   const int nblk = gridDim.x / g.in_px;
-  for (int band = blockIdx.x / g.in_px; band < nbands_total; band += nblk) {
+  for (int unit = blockIdx.x / g.in_px; unit < nbands_total * nseg; unit += nblk) {
+    const int band = unit / nseg;
+    const int x_begin = (unit - band * nseg) * segw, x_end = min(g.W, x_begin + segw);
+    const int qtotal = (x_end - x_begin) - xs + t.pmax;  // virtual columns q = x - x_begin - xs
+    const int nin = (qtotal + CW - 1) / CW;
+    const int nout = (x_end - x_begin + CW - 1) / CW;
     const long long row0 = (long long)band * HB;
     const int nrows = (int)min((long long)HB, (long long)g.nimg * g.H - row0);
     if (producer) {
@@ -2349,7 +2355,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
       }
       const bool vec = g.aligned16 && g.in_px == 1;
       auto issue = [&](int j, int buf) {
-        const int xq0 = xs + j * CW;  // 16-aligned first column of chunk j
+        const int xq0 = x_begin + xs + j * CW;  // 16-aligned first column of chunk j
         if (vec && xq0 >= 0 && xq0 + CW <= g.W) {
           // interior chunk: 16-byte copies, 8 rows x VPR vectors (xq0 is a multiple of 16 columns)
           constexpr int VPR = CW * (int)sizeof(Tin) / 16;
@@ -2462,11 +2468,11 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h >= no) break;
-          const int x = (o + h) * CW + c;
+          const int x = x_begin + (o + h) * CW + c;
 #pragma unroll
           for (int i = 0; i < K; ++i) {
-            const int* pl = P + r0 * RLS + ((x - xs + t.p[i]) & (RL - 1));
-            const int* pt = P + r0 * RLS + ((x - xs - t.p[i] - 1) & (RL - 1));
+            const int* pl = P + r0 * RLS + ((x - x_begin - xs + t.p[i]) & (RL - 1));
+            const int* pt = P + r0 * RLS + ((x - x_begin - xs - t.p[i] - 1) & (RL - 1));
             const float2 w2 = make_float2(t.w_row[i], t.w_row[i]);
 #pragma unroll
             for (int r = 0; r < SHB / 2; ++r) {
@@ -2485,8 +2491,8 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h >= no) break;
-          const int x = (o + h) * CW + c;
-          if (x < g.W) {
+          const int x = x_begin + (o + h) * CW + c;
+          if (x < x_end) {
             if (whole) {
               // 32-bit element offsets from the band's first row (HB plane rows < 2^31 elements):
               // one IMAD.WIDE per store instead of a 64-bit pointer chain
@@ -2531,7 +2537,7 @@ constexpr int mc_rows(int C) { return (HB + C - 1) / C + 1; }
 template <typename Tin, int K>
 __global__ void __launch_bounds__(STREAM_THREADS, 2)
     stream_rows_mc_kernel(const Tin* __restrict__ src, int* __restrict__ mid_out, Geometry g, Taps t, int xs,
-                          int nbands_total, int* status) {
+                          int nbands_total, int segw, int* status) {
   static_assert(SRG == 1, "the interleaved streaming row pass assumes one consumer row group");
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
@@ -2542,9 +2548,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
   const int warp = threadIdx.x >> 5;
   const bool producer = warp >= SCONS;
   const int C = g.in_px;
-  const int qtotal = g.W - xs + t.pmax;
-  const int nin = (qtotal + CW - 1) / CW;
-  const int nout = (g.W + CW - 1) / CW;
+  const int nseg = (g.W + segw - 1) / segw;  // column segments per band (see stream_rows_kernel)
   const int lagc = (CW - 1 - xs + t.pmax) / CW;
   const int ntmax = (HB + C - 1) / C + 1;
   const int srb = CW * C * ES + SRB_PAD;      // staged image row: CW pixels of C elements (+ 16 bytes)
@@ -2562,7 +2566,12 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
   const long long tall = (long long)g.nimg * g.H;
   const long long VR = tall * C;  // virtual rows
   uint32_t cin_ctr = 0, out_ctr = 0;
-  for (int band = blockIdx.x; band < nbands_total; band += gridDim.x) {
+  for (int unit = blockIdx.x; unit < nbands_total * nseg; unit += gridDim.x) {
+    const int band = unit / nseg;
+    const int x_begin = (unit - band * nseg) * segw, x_end = min(g.W, x_begin + segw);
+    const int qtotal = (x_end - x_begin) - xs + t.pmax;
+    const int nin = (qtotal + CW - 1) / CW;
+    const int nout = (x_end - x_begin + CW - 1) / CW;
     const long long vr0 = (long long)band * HB;
     const int nrows = (int)min((long long)HB, VR - vr0);
     const long long t_first = vr0 / C;
@@ -2582,11 +2591,11 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
       // filtering.py:10-13): 4-byte cp.async by all producer threads, waited for as a group; the
       // issuing thread completes the phase by a plain arrive so every buffer use is one phase.
       auto interior = [&](int j) {
-        const int xq0 = xs + j * CW;  // 16-aligned first column of chunk j
+        const int xq0 = x_begin + xs + j * CW;  // 16-aligned first column of chunk j
         return xq0 >= 0 && xq0 + CW <= g.W;
       };
       auto issue = [&](int j) {
-        const int xq0 = xs + j * CW;
+        const int xq0 = x_begin + xs + j * CW;
         const int buf = (int)((cin_ctr + (uint32_t)j) % STG);
         unsigned char* sbuf = stage + buf * ntmax * srb;
         if (interior(j)) {
@@ -2673,11 +2682,11 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h >= no) break;
-          const int x = (o + h) * CW + c;
+          const int x = x_begin + (o + h) * CW + c;
 #pragma unroll
           for (int i = 0; i < K; ++i) {
-            const int* pl = P + ((x - xs + t.p[i]) & (RL - 1));
-            const int* pt = P + ((x - xs - t.p[i] - 1) & (RL - 1));
+            const int* pl = P + ((x - x_begin - xs + t.p[i]) & (RL - 1));
+            const int* pt = P + ((x - x_begin - xs - t.p[i] - 1) & (RL - 1));
             const float2 w2 = make_float2(t.w_row[i], t.w_row[i]);
 #pragma unroll
             for (int r = 0; r < HB / 2; ++r) {
@@ -2696,8 +2705,8 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h >= no) break;
-          const int x = (o + h) * CW + c;
-          if (x < g.W) {
+          const int x = x_begin + (o + h) * CW + c;
+          if (x < x_end) {
             int off = off0 + x, cc = c_first;
 #pragma unroll
             for (int r = 0; r < HB / 2; ++r) {

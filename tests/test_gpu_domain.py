@@ -318,3 +318,31 @@ def test_interleaved_channels_every_source_type(dtype, shape, k, sigma):
         for c in range(shape[3]):
             ref = O.separable_filter_2d(np.ascontiguousarray(x[n, :, :, c]), kern.radii, kern.weights)
             assert float(np.abs(got[n, :, :, c] - ref).max()) * 255.0 / scale <= BAR
+
+
+# Column segments of the streaming row pass: images with few rows and long rows are cut into
+# (band, segment) units, each segment re-scanning its own halo - the result must not change.
+@pytest.mark.parametrize("dtype,shape,k,sigma", [
+    (np.float32, (1, 150, 6000), 4, 30.0),
+    (np.float32, (1, 130, 5003), 4, 20.0),       # width not a multiple of the chunk or of 16
+    (np.uint8, (1, 140, 4096, 3), 4, 20.0),      # interleaved channels, bulk-copy staging
+    (np.float64, (2, 90, 4100), 3, 25.0),
+], ids=["f32", "f32-odd-width", "u8-rgb", "f64-batch"])
+def test_streaming_rows_column_segments(dtype, shape, k, sigma):
+    rng = np.random.default_rng(shape[2])
+    x = (rng.random(shape) * 255).astype(dtype)
+    kern = A.table_kernel(k, sigma)
+    assert 31 < kern.max_radius < shape[1]
+    cl = len(shape) == 4
+    bound = None if dtype == np.uint8 else 255.0
+    xt = torch.from_numpy(x).cuda()
+    got = F.separable_filter_batch(xt, kern, channels_last=cl, value_bound=bound).cpu().numpy()
+    with nat.path_policy(nat.SB_PATH_GENERIC):
+        gen = F.separable_filter_batch(xt, kern, channels_last=cl, value_bound=bound).cpu().numpy()
+    np.testing.assert_array_equal(got, gen)
+    for n in range(shape[0]):
+        for c in range(shape[3] if cl else 1):
+            img = np.ascontiguousarray(x[n, :, :, c] if cl else x[n])
+            ref = O.separable_filter_2d(img, kern.radii, kern.weights)
+            res = got[n, :, :, c] if cl else got[n]
+            assert float(np.abs(res - ref).max()) <= BAR
