@@ -2302,7 +2302,22 @@ constexpr int SCONS = SRG * (CW / 32);
 constexpr int STREAM_THREADS = 32 * (SCONS + NPROD);
 constexpr int SHB = HB / SRG;  // rows per consumer thread
 
-template <typename Tin, int K>
+// The two words a consumer stores for a row pair: the row values rounded to the mid quantum
+// (int32 plane), or their float bits (row pass alone).
+template <int K, bool TO_OUT>
+__device__ __forceinline__ int2 plane_words(float2 rv) {
+  if constexpr (TO_OUT) {
+    return make_int2(__float_as_int(rv.x), __float_as_int(rv.y));
+  } else {
+    const float2 q = round_mid2<K>(rv);  // round to the mid quantum
+    return make_int2(__float_as_int(q.x) - kMagicBits, __float_as_int(q.y) - kMagicBits);
+  }
+}
+
+// TO_OUT: the row pass alone (`_filter_rows`, filtering.py:48-64): weights in pixel units and
+// the float row values stored as they are (mid_out is then the float destination, g.mid_row its
+// row stride), exactly as rows_kernel<.., RowsToOut> forms them.
+template <typename Tin, int K, bool TO_OUT = false>
 __global__ void __launch_bounds__(STREAM_THREADS, 2)
     stream_rows_kernel(const Tin* __restrict__ src, int* __restrict__ mid_out, Geometry g, Taps t, int xs,
                        int nbands_total, int segw, int* status) {
@@ -2473,7 +2488,8 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
           for (int i = 0; i < K; ++i) {
             const int* pl = P + r0 * RLS + ((x - x_begin - xs + t.p[i]) & (RL - 1));
             const int* pt = P + r0 * RLS + ((x - x_begin - xs - t.p[i] - 1) & (RL - 1));
-            const float2 w2 = make_float2(t.w_row[i], t.w_row[i]);
+            const float wi = TO_OUT ? t.w_out1[i] : t.w_row[i];
+            const float2 w2 = make_float2(wi, wi);
 #pragma unroll
             for (int r = 0; r < SHB / 2; ++r) {
               const float2 d = make_float2(i2f_fast((uint32_t)(pl[2 * r * RLS] - pt[2 * r * RLS])),
@@ -2500,17 +2516,17 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
               int idx = x;
 #pragma unroll
               for (int r = 0; r < SHB / 2; ++r) {
-                const float2 q = round_mid2<K>(rv[h][r]);  // round to the mid quantum
-                st_global_idx(mid0g, idx, __float_as_int(q.x) - kMagicBits);
-                st_global_idx(mid0g, idx + ms, __float_as_int(q.y) - kMagicBits);
+                const int2 q = plane_words<K, TO_OUT>(rv[h][r]);
+                st_global_idx(mid0g, idx, q.x);
+                st_global_idx(mid0g, idx + ms, q.y);
                 idx += 2 * ms;
               }
             } else {
 #pragma unroll
               for (int r = 0; r < SHB / 2; ++r) {
-                const float2 q = round_mid2<K>(rv[h][r]);
-                if (r0 + 2 * r < nrows) midrow_of(r0 + 2 * r)[x] = __float_as_int(q.x) - kMagicBits;
-                if (r0 + 2 * r + 1 < nrows) midrow_of(r0 + 2 * r + 1)[x] = __float_as_int(q.y) - kMagicBits;
+                const int2 q = plane_words<K, TO_OUT>(rv[h][r]);
+                if (r0 + 2 * r < nrows) midrow_of(r0 + 2 * r)[x] = q.x;
+                if (r0 + 2 * r + 1 < nrows) midrow_of(r0 + 2 * r + 1)[x] = q.y;
               }
             }
           }
@@ -2743,6 +2759,20 @@ const void* stream_mc_ptr_for(int k) {
   }
 }
 
+template <typename Tin>
+const void* stream_out_ptr_for(int k) {
+  switch (k) {
+    case 1: return (const void*)stream_rows_kernel<Tin, 1, true>;
+    case 2: return (const void*)stream_rows_kernel<Tin, 2, true>;
+    case 3: return (const void*)stream_rows_kernel<Tin, 3, true>;
+    case 4: return (const void*)stream_rows_kernel<Tin, 4, true>;
+    case 5: return (const void*)stream_rows_kernel<Tin, 5, true>;
+    case 6: return (const void*)stream_rows_kernel<Tin, 6, true>;
+    case 7: return (const void*)stream_rows_kernel<Tin, 7, true>;
+    default: return (const void*)stream_rows_kernel<Tin, 8, true>;
+  }
+}
+
 template <typename Tin>  // a template: instantiates its kernels only where it is called
 const void* stream_ptr_for(int k) {
 #define SB_STREAM(KK) stream_rows_kernel<Tin, KK>
@@ -2785,6 +2815,7 @@ const void* sweep_ptr_stream_f64(int k);  // streaming row pass, one-channel flo
 const void* sweep_ptr_stream_u8(int k);
 const void* sweep_ptr_stream_u16(int k);
 const void* sweep_ptr_stream_mc(int src_dtype, int k);  // streaming row pass, interleaved channels staged once
+const void* sweep_ptr_stream_out(int src_dtype, int k); // streaming row pass alone (float rows out), one channel
 const void* sweep_ptr_fused3(int k);      // fused sweep, three CTAs per SM (uint8, one channel)
 const void* sweep_ptr_fused5(int k);      // fused sweep, two bands per consumer iteration (uint8, one channel)
 const void* sweep_ptr_fusedp(int k);      // fused sweep, paired consumer warps (uint8, one channel)

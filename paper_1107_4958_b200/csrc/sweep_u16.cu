@@ -17,4 +17,14 @@ const void* sweep_ptr_stream_mc(int src_dtype, int k) {
     default: return sweep_ptr_stream_mc_f64(k);
   }
 }
+const void* sweep_ptr_stream_out_f32(int k);
+const void* sweep_ptr_stream_out_f64(int k);
+const void* sweep_ptr_stream_out(int src_dtype, int k) {
+  switch (src_dtype) {
+    case SB_DTYPE_U8: return stream_out_ptr_for<uint8_t>(k);
+    case SB_DTYPE_U16: return stream_out_ptr_for<uint16_t>(k);
+    case SB_DTYPE_F32: return sweep_ptr_stream_out_f32(k);
+    default: return sweep_ptr_stream_out_f64(k);
+  }
+}
 }  // namespace sb
