@@ -316,6 +316,9 @@ constexpr size_t kCols2Smem = (size_t)SB_COLS2_SMEM_KB * 1024;
 #ifndef SB_STREAM_MC
 #define SB_STREAM_MC 1
 #endif
+#ifndef SB_STREAM_MC_UNALIGNED
+#define SB_STREAM_MC_UNALIGNED 1
+#endif
 #ifndef SB_STREAM_ROWS_OUT
 #define SB_STREAM_ROWS_OUT 1
 #endif
@@ -729,9 +732,11 @@ int stream_segment_width(int64_t width, int pmax, long long par_bands, int sms) 
 bool stream_rows_fits(int src_dtype, int pmax, int channels, int64_t width) {
   const int xs = -(((pmax + 1) + 15) & ~15);
   const int lagc = (sb::CW - 1 - xs + pmax) / sb::CW;
-  // interleaved channels of the other types: only rows the bulk copies can stage (16-byte multiples)
+  // interleaved channels of the other types: up to four (stream_rows_mc_kernel; rows that are not
+  // 16-byte multiples are staged from aligned-down addresses)
   const bool other = SB_STREAM_ALL_TYPES &&
-                     (channels == 1 || (channels <= 4 && (width * channels * dtype_size(src_dtype)) % 16 == 0));
+                     (channels == 1 || (channels <= 4 && (SB_STREAM_MC_UNALIGNED ||
+                                                          (width * channels * dtype_size(src_dtype)) % 16 == 0)));
   return (src_dtype == SB_DTYPE_F32 || other) && lagc + 1 < sb::NSLOT;
 }
 
@@ -1021,16 +1026,19 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     const int xs = -(((plan.pmax + 1) + 15) & ~15);  // first halo column, 16-aligned
     // interleaved channels with 16-byte aligned rows: bands of virtual (row, channel) rows, the
     // image rows staged once for all channels (stream_rows_mc_kernel); else one channel per CTA
-    const bool mc = SB_STREAM_MC && channels >= 2 && channels <= 4 && g.in_px == channels && g.aligned16 &&
-                    (width * channels * g.es) % 16 == 0 && all_rows * width * channels < (1LL << 31) &&
-                    (src_dtype == SB_DTYPE_F32 || SB_STREAM_ALL_TYPES);
+    // rows that are not 16-byte multiples are staged from aligned-down addresses (unal); the
+    // first image row must be 16-byte aligned so no copy starts before the caller's buffer
+    const int unal = (g.in_row * g.es) % 16 != 0 || (g.in_img * g.es) % 16 != 0;
+    const bool mc = SB_STREAM_MC && channels >= 2 && channels <= 4 && g.in_px == channels &&
+                    (uintptr_t)src % 16 == 0 && (!unal || SB_STREAM_MC_UNALIGNED) &&
+                    all_rows * width * channels < (1LL << 31) && (src_dtype == SB_DTYPE_F32 || SB_STREAM_ALL_TYPES);
     const void* fs = mc                            ? sb::sweep_ptr_stream_mc(src_dtype, k)
                      : src_dtype == SB_DTYPE_F32   ? sb::sweep_ptr_stream_f32(k)
                      : src_dtype == SB_DTYPE_F64   ? sb::sweep_ptr_stream_f64(k)
                      : src_dtype == SB_DTYPE_U16   ? sb::sweep_ptr_stream_u16(k)
                                                    : sb::sweep_ptr_stream_u8(k);
     const size_t stage = mc ? (size_t)sb::stream_stages(g.es) * sb::mc_rows(channels) *
-                                  (sb::CW * channels * (size_t)g.es + sb::SRB_PAD)
+                                  (sb::CW * channels * (size_t)g.es + sb::SRB_PAD + (unal ? 16 : 0))
                             : (size_t)sb::NPROD * sb::stream_stages(g.es) * 8 * (sb::CW * (size_t)g.es + sb::SRB_PAD);
     const size_t smem = stage + (size_t)sb::HB * sb::RLS * sizeof(int);
     FnFacts ff;
@@ -1046,8 +1054,11 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     const int units_total = nb_total * (int)((width + segw - 1) / segw);
     const int gx = mc ? std::max(1, std::min(units_total, df.sms * 2 * 8))
                       : std::max(1, std::min(units_total, df.sms * 2 * 8 / std::max(1, channels)));
-    void* args[] = {(void*)&src, (void*)&mid, (void*)&g, (void*)&plan.taps, (void*)&xs, (void*)&nb_total,
-                    (void*)&segw, (void*)&status_dev};
+    void* args_mc[] = {(void*)&src, (void*)&mid, (void*)&g, (void*)&plan.taps, (void*)&xs, (void*)&nb_total,
+                       (void*)&segw, (void*)&unal, (void*)&status_dev};
+    void* args_1c[] = {(void*)&src, (void*)&mid, (void*)&g, (void*)&plan.taps, (void*)&xs, (void*)&nb_total,
+                       (void*)&segw, (void*)&status_dev};
+    void** args = mc ? args_mc : args_1c;
     if (debug_plans())
       std::fprintf(stderr, "[sliceblur_b200] stream rows: pmax=%d xs=%d bands=%d segw=%d grid=%d x %d smem=%zu\n",
                    plan.pmax, xs, nb_total, segw, gx, channels, smem);

@@ -2553,7 +2553,7 @@ constexpr int mc_rows(int C) { return (HB + C - 1) / C + 1; }
 template <typename Tin, int K>
 __global__ void __launch_bounds__(STREAM_THREADS, 2)
     stream_rows_mc_kernel(const Tin* __restrict__ src, int* __restrict__ mid_out, Geometry g, Taps t, int xs,
-                          int nbands_total, int segw, int* status) {
+                          int nbands_total, int segw, int unal, int* status) {
   static_assert(SRG == 1, "the interleaved streaming row pass assumes one consumer row group");
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_done[NSLOT];
@@ -2561,13 +2561,19 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
   constexpr int ES = (int)sizeof(Tin);
   __shared__ __align__(8) uint64_t sfull[STG];  // staged chunk landed (bulk-copy bytes / edge-chunk arrive)
   __shared__ const Tin* rowp_s[HB / 2 + 2];     // the band's image rows (clamped at the end of the tall image)
+  // unal: image rows that are not 16-byte multiples.  Row i is then staged from its chunk start
+  // rounded down to 16 bytes (rowsh_s[i] bytes early, the same for every chunk of the row) and
+  // padded to 16 bytes behind, so the bulk copies stay aligned; the scan skips the shift.  A
+  // chunk counts as interior only if the padding still lies inside the image row.
+  __shared__ int rowsh_s[HB / 2 + 2];
   const int warp = threadIdx.x >> 5;
   const bool producer = warp >= SCONS;
   const int C = g.in_px;
   const int nseg = (g.W + segw - 1) / segw;  // column segments per band (see stream_rows_kernel)
   const int lagc = (CW - 1 - xs + t.pmax) / CW;
   const int ntmax = (HB + C - 1) / C + 1;
-  const int srb = CW * C * ES + SRB_PAD;      // staged image row: CW pixels of C elements (+ 16 bytes)
+  const int srb = CW * C * ES + SRB_PAD + (unal ? 16 : 0);  // staged image row: CW pixels of C elements (+ padding)
+  const int pad_px = unal ? (16 + C * ES - 1) / (C * ES) : 0;
   unsigned char* stage = smem;                // [STG][ntmax][srb]
   int* P = (int*)(smem + STG * ntmax * srb);  // [HB][RLS]
   if (threadIdx.x == 0) {
@@ -2598,7 +2604,9 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
       if (ptid < nt) {
         const long long tt = t_first + ptid;
         const int img = (int)(tt / g.H), v = (int)(tt - (long long)img * g.H);
-        rowp_s[ptid] = src + (long long)img * g.in_img + (long long)v * g.in_row;
+        const Tin* rp = src + (long long)img * g.in_img + (long long)v * g.in_row;
+        rowp_s[ptid] = rp;
+        rowsh_s[ptid] = unal ? (int)((size_t)rp & 15) : 0;
       }
       named_bar_sync(1, 32 * NPROD);
       // Chunk gc (counted over the CTA's bands) lives in staging buffer gc % STG; its landing is
@@ -2608,7 +2616,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
       // issuing thread completes the phase by a plain arrive so every buffer use is one phase.
       auto interior = [&](int j) {
         const int xq0 = x_begin + xs + j * CW;  // 16-aligned first column of chunk j
-        return xq0 >= 0 && xq0 + CW <= g.W;
+        return xq0 >= 0 && xq0 + CW + pad_px <= g.W;
       };
       auto issue = [&](int j) {
         const int xq0 = x_begin + xs + j * CW;
@@ -2616,9 +2624,12 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
         unsigned char* sbuf = stage + buf * ntmax * srb;
         if (interior(j)) {
           if (ptid == 0) {
-            mbar_expect_tx(&sfull[buf], (uint32_t)(nt * CW * C * ES));
+            uint32_t tx = 0;
+            for (int i = 0; i < nt; ++i) tx += (uint32_t)((rowsh_s[i] + CW * C * ES + 15) & ~15);
+            mbar_expect_tx(&sfull[buf], tx);
             for (int i = 0; i < nt; ++i)
-              bulk_g2s(sbuf + i * srb, rowp_s[i] + (long long)xq0 * C, (uint32_t)(CW * C * ES), &sfull[buf]);
+              bulk_g2s(sbuf + i * srb, (const unsigned char*)(rowp_s[i] + (long long)xq0 * C) - rowsh_s[i],
+                       (uint32_t)((rowsh_s[i] + CW * C * ES + 15) & ~15), &sfull[buf]);
           }
         } else {
           for (int i = 0; i < nt; ++i) {
@@ -2627,10 +2638,11 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
               const int px = e / C, cc = e - px * C;
               const int x = min(max(xq0 + px, 0), g.W - 1);
               if constexpr (ES == 4)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(sbuf + i * srb + 4 * e)),
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                                 smem_u32(sbuf + i * srb + rowsh_s[i] + 4 * e)),
                              "l"(rp + (long long)x * C + cc));
               else
-                *(Tin*)(sbuf + i * srb + ES * e) = rp[(long long)x * C + cc];  // visible after the named barrier
+                *(Tin*)(sbuf + i * srb + rowsh_s[i] + ES * e) = rp[(long long)x * C + cc];  // visible after the named barrier
             }
           }
           cp_async_commit();
@@ -2641,7 +2653,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
       const int rr = lane & 7;
       const long long vr = vr0 + min(8 * pw + rr, nrows - 1);
       const long long tt = vr / C;
-      const int lane_off = (int)(tt - t_first) * srb + (int)(vr - tt * C) * ES;
+      const int lane_off = (int)(tt - t_first) * srb + rowsh_s[(int)(tt - t_first)] + (int)(vr - tt * C) * ES;
       int carry = 0;
       for (int j = 0; j < STG - 1 && j < nin; ++j) issue(j);
       RangeAcc bad;

@@ -300,8 +300,13 @@ def test_streaming_rows_every_source_type(dtype, shape, k, sigma):
     (np.uint16, (1, 200, 264, 3), 4, 30.0),
     (np.float64, (1, 333, 274, 3), 4, 40.0),
     (np.float64, (2, 120, 300, 2), 3, 25.0),
-    (np.uint8, (1, 200, 333, 3), 4, 20.0),    # rows not 16-byte multiples: tiled row pass
-], ids=["u8-rgb", "u8-rgba-large", "u8-rgb-short", "u16-rgb", "f64-rgb", "f64-2ch", "u8-rgb-unaligned"])
+    (np.uint8, (1, 200, 333, 3), 4, 20.0),    # rows not 16-byte multiples: staged from aligned-down addresses
+    (np.uint8, (3, 75, 1001, 3), 4, 12.0),    # ... several images (image stride not a 16-byte multiple either)
+    (np.float64, (2, 90, 301, 3), 3, 25.0),
+    (np.uint16, (2, 60, 203, 2), 4, 8.0),
+    (np.float32, (2, 130, 515, 3), 5, 30.0),
+], ids=["u8-rgb", "u8-rgba-large", "u8-rgb-short", "u16-rgb", "f64-rgb", "f64-2ch", "u8-rgb-unaligned",
+        "u8-rgb-unaligned-batch", "f64-rgb-unaligned", "u16-2ch-unaligned", "f32-rgb-unaligned"])
 def test_interleaved_channels_every_source_type(dtype, shape, k, sigma):
     rng = np.random.default_rng(shape[1] * shape[2])
     scale = 65535 if dtype == np.uint16 else 255
@@ -311,9 +316,12 @@ def test_interleaved_channels_every_source_type(dtype, shape, k, sigma):
     bound = None if dtype in (np.uint8, np.uint16) else float(scale)
     xt = torch.from_numpy(x).cuda()
     got = F.separable_filter_batch(xt, kern, channels_last=True, value_bound=bound).cpu().numpy()
+    with nat.path_policy(nat.SB_PATH_UNFUSED):  # small radii: force the streaming row pass
+        unf = F.separable_filter_batch(xt, kern, channels_last=True, value_bound=bound).cpu().numpy()
     with nat.path_policy(nat.SB_PATH_GENERIC):
         gen = F.separable_filter_batch(xt, kern, channels_last=True, value_bound=bound).cpu().numpy()
     np.testing.assert_array_equal(got, gen)
+    np.testing.assert_array_equal(unf, gen)
     for n in range(shape[0]):
         for c in range(shape[3]):
             ref = O.separable_filter_2d(np.ascontiguousarray(x[n, :, :, c]), kern.radii, kern.weights)
