@@ -705,6 +705,12 @@ bool needs_wide(int pmax) { return 2LL * pmax + 1 > sb::kWideSpan; }
 
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
+// stream_rows_kernel's `unal` mode (one channel, rows not 16-byte multiples, aligned base):
+// staged rows carry one more 16-byte vector
+bool stream_unaligned(const void* src, const sb::Geometry& g) {
+  return g.in_px == 1 && !g.aligned16 && ((uintptr_t)src & 15) == 0;
+}
+
 // Segment width (a multiple of the chunk) of the streaming row pass: the segment count that
 // minimises (rounds of units over the resident CTAs, two per SM) x (segment + halo width).
 int stream_segment_width(int64_t width, int pmax, long long par_bands, int sms) {
@@ -770,7 +776,14 @@ Route route_2d(int src_dtype, int64_t width, int channels, const int64_t* radii,
   const bool u8_unpacked = SB_STREAM_ALL_TYPES && src_dtype == SB_DTYPE_U8 && channels == 1 &&
                            !make_tiling(sb::Mode::Fused, pmax, 1, 1, true).packed &&
                            stream_rows_fits(src_dtype, pmax, channels, width);
-  if (fast && g_policy != SB_PATH_UNFUSED && fused_fits(pmax, channels, es) && !u8_unpacked) {
+  // Dense rows that are not 16-byte multiples: the fused sweep stages them element by element
+  // (4001^2 float32 p_max 20: 0.224 ms), the streaming row pass from aligned-down 16-byte copies
+  // (0.128 ms); packed uint8 stays fused (64 x 1000^2: 0.43 vs 0.56 ms; a pitched device copy
+  // into an aligned layout first measured 0.36 ms and is not used).
+  const bool unaligned_rows = SB_STREAM_ALL_TYPES && (width * channels * es) % 16 != 0 &&
+                              !(src_dtype == SB_DTYPE_U8 && channels == 1) &&
+                              stream_rows_fits(src_dtype, pmax, channels, width);
+  if (fast && g_policy != SB_PATH_UNFUSED && fused_fits(pmax, channels, es) && !u8_unpacked && !unaligned_rows) {
     r.rows = RowPath::Fused;
     r.cols = ColPath::None;
     return r;
@@ -876,13 +889,17 @@ int sb_check_kernel(const int64_t* radii, const double* weights, int k, int64_t 
   return SB_OK;
 }
 
+// Row pitch (elements) of the intermediate plane: the width rounded up to four elements, so plane
+// rows are 16-byte multiples for every image width (cols2_kernel's TMA loads need that)
+static int64_t plane_width(int64_t width) { return (width + 3) & ~(int64_t)3; }
+
 size_t sb_separable_filter_2d_workspace_bytes(int src_dtype, int64_t batch, int64_t height, int64_t width,
                                               int channels, const int64_t* radii, int k) {
   if (!radii || k < 1 || k > SB_MAX_K || batch < 1 || height < 1 || width < 1 || channels < 1) return 0;
   if (dtype_size(src_dtype) == 0 || radii[k - 1] < 0 || radii[k - 1] > 0x7fffffff) return 0;
   const Route r = route_2d(src_dtype, width, channels, radii, k);
   if (r.rows == RowPath::Fused || r.rows == RowPath::FusedWide || r.rows == RowPath::RowTile) return 0;
-  const size_t plane = (size_t)batch * height * width * channels * (r.wide ? sizeof(long long) : sizeof(int));
+  const size_t plane = (size_t)batch * height * plane_width(width) * channels * (r.wide ? sizeof(long long) : sizeof(int));
   return r.scratch_bytes ? align256(plane) + r.scratch_bytes : plane;
 }
 
@@ -1015,8 +1032,8 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
   if (!workspace || workspace_bytes < need)
     return fail(SB_ERR_WORKSPACE, "workspace of " + std::to_string(need) + " bytes required");
   int* mid = (int*)workspace;
-  g.mid_row = width;
-  g.mid_img = (long long)height * width;
+  g.mid_row = (long long)plane_width(width);  // rows padded to 16 bytes: the plane keeps its TMA tensor map
+  g.mid_img = (long long)height * g.mid_row;
   g.mid_ch = g.mid_img * batch;
   const int sms = device_sms();
 
@@ -1031,7 +1048,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     const int unal = (g.in_row * g.es) % 16 != 0 || (g.in_img * g.es) % 16 != 0;
     const bool mc = SB_STREAM_MC && channels >= 2 && channels <= 4 && g.in_px == channels &&
                     (uintptr_t)src % 16 == 0 && (!unal || SB_STREAM_MC_UNALIGNED) &&
-                    all_rows * width * channels < (1LL << 31) && (src_dtype == SB_DTYPE_F32 || SB_STREAM_ALL_TYPES);
+                    all_rows * g.mid_row * channels < (1LL << 31) && (src_dtype == SB_DTYPE_F32 || SB_STREAM_ALL_TYPES);
     const void* fs = mc                            ? sb::sweep_ptr_stream_mc(src_dtype, k)
                      : src_dtype == SB_DTYPE_F32   ? sb::sweep_ptr_stream_f32(k)
                      : src_dtype == SB_DTYPE_F64   ? sb::sweep_ptr_stream_f64(k)
@@ -1039,7 +1056,8 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
                                                    : sb::sweep_ptr_stream_u8(k);
     const size_t stage = mc ? (size_t)sb::stream_stages(g.es) * sb::mc_rows(channels) *
                                   (sb::CW * channels * (size_t)g.es + sb::SRB_PAD + (unal ? 16 : 0))
-                            : (size_t)sb::NPROD * sb::stream_stages(g.es) * 8 * (sb::CW * (size_t)g.es + sb::SRB_PAD);
+                            : (size_t)sb::NPROD * sb::stream_stages(g.es) * 8 *
+                                  (sb::CW * (size_t)g.es + sb::SRB_PAD + (stream_unaligned(src, g) ? 16 : 0));
     const size_t smem = stage + (size_t)sb::HB * sb::RLS * sizeof(int);
     FnFacts ff;
     DevFacts df;
@@ -1074,7 +1092,7 @@ int sb_separable_filter_2d_window(const void* src, int src_dtype, int64_t batch,
     if (rc) return rc;
   } else {
     const size_t plane =
-        (size_t)batch * height * width * channels * (route.wide ? sizeof(long long) : sizeof(int));
+        (size_t)batch * height * plane_width(width) * channels * (route.wide ? sizeof(long long) : sizeof(int));
     void* scratch = route.scratch_bytes ? (void*)((char*)workspace + align256(plane)) : nullptr;
     if (debug_plans())
       std::fprintf(stderr, "[sliceblur_b200] generic rows: pmax=%d k=%d W=%d wide=%d scratch=%zu\n", plan.pmax, k,
@@ -1185,7 +1203,8 @@ int sb_filter_rows(const void* src, int src_dtype, int64_t rows, int64_t width, 
     // the streaming row pass with float rows out (8192^2 sigma 64: float32 0.85 -> 0.21 ms, float64 2.08 -> 0.28 ms)
     const int xs = -(((plan.pmax + 1) + 15) & ~15);
     const void* fs = sb::sweep_ptr_stream_out(src_dtype, k);
-    const size_t smem = (size_t)sb::NPROD * sb::stream_stages(g.es) * 8 * (sb::CW * (size_t)g.es + sb::SRB_PAD) +
+    const size_t smem = (size_t)sb::NPROD * sb::stream_stages(g.es) * 8 *
+                            (sb::CW * (size_t)g.es + sb::SRB_PAD + (stream_unaligned(src, g) ? 16 : 0)) +
                         (size_t)sb::HB * sb::RLS * sizeof(int);
     FnFacts ff;
     DevFacts df;

@@ -2334,7 +2334,14 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
   const int lagc = (CW - 1 - xs + t.pmax) / CW;
   // staged rows and prefix-ring rows are an odd multiple of 16 bytes apart, so the 8 lanes
   // of a 128-bit access phase (8 rows, same chunk) hit 8 distinct bank groups
-  const int rowbytes = CW * (int)sizeof(Tin) + SRB_PAD;
+  // unal: one channel, rows that are not 16-byte multiples, 16-byte aligned base.  A row's
+  // chunk is then staged from its start rounded down to 16 bytes (VPR + 1 vectors; the shift is
+  // the same for every chunk of the row) and the scan reads element by element behind the
+  // shift; a chunk is interior only while the extra vector lies inside the image row.
+  const bool unal = g.in_px == 1 && !g.aligned16 && ((size_t)src & 15) == 0;
+  const int rowbytes = CW * (int)sizeof(Tin) + SRB_PAD + (unal ? 16 : 0);
+  const int pad_el = unal ? (16 + (int)sizeof(Tin) - 1) / (int)sizeof(Tin) : 0;
+  __shared__ const Tin* rowp_sh[NPROD][8];
   unsigned char* stage = smem;                           // [NPROD][STG][8][rowbytes]
   int* P = (int*)(smem + NPROD * STG * 8 * rowbytes);    // [HB][RLS]
 
@@ -2369,6 +2376,18 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
         rowp[rr] = src + (long long)img * g.in_img + (long long)v * g.in_row + ch;
       }
       const bool vec = g.aligned16 && g.in_px == 1;
+      if (unal) {
+        __syncwarp();
+        if (lane < 8) {
+          const long long trow = row0 + min(8 * pw + lane, nrows - 1);
+          const int img = (int)(trow / g.H), v = (int)(trow - (long long)img * g.H);
+          rowp_sh[pw][lane] = src + (long long)img * g.in_img + (long long)v * g.in_row;
+        }
+        __syncwarp();
+      }
+      // this lane's row starts (size_t)row & 15 bytes behind a 16-byte boundary (chunk starts are
+      // 16-column multiples, so the shift does not depend on the chunk)
+      const int mysh = unal ? (int)((size_t)rowp_sh[pw][lane & 7] & 15) : 0;
       auto issue = [&](int j, int buf) {
         const int xq0 = x_begin + xs + j * CW;  // 16-aligned first column of chunk j
         if (vec && xq0 >= 0 && xq0 + CW <= g.W) {
@@ -2381,10 +2400,17 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
             cp_async16(mystage + (buf * 8 + rr) * rowbytes + 16 * e4,
                        (const unsigned char*)(rowp[rr] + xq0) + 16 * e4);
           }
+        } else if (unal && xq0 >= 0 && xq0 + CW + pad_el <= g.W) {
+          constexpr int VPR1 = CW * (int)sizeof(Tin) / 16 + 1;
+          for (int idx = lane; idx < 8 * VPR1; idx += 32) {
+            const int rr = idx / VPR1, e4 = idx - rr * VPR1;
+            const unsigned char* a = (const unsigned char*)(rowp_sh[pw][rr] + xq0);
+            cp_async16(mystage + (buf * 8 + rr) * rowbytes + 16 * e4, a - ((size_t)a & 15) + 16 * e4);
+          }
         } else {
 #pragma unroll
           for (int rr = 0; rr < 8; ++rr) {
-            Tin* sp = (Tin*)(mystage + (buf * 8 + rr) * rowbytes);
+            Tin* sp = (Tin*)(mystage + (buf * 8 + rr) * rowbytes + (unal ? (int)((size_t)rowp[rr] & 15) : 0));
             for (int e = lane; e < CW; e += 32) {
               const int x = min(max(xq0 + e, 0), g.W - 1);  // replicate border columns
               const Tin* gp = rowp[rr] + (long long)x * g.in_px;
@@ -2435,9 +2461,15 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
             uint4 q[CH * sizeof(Tin) / 16];
             Tin e[CH];
           } u;
-          const uint4* ep = (const uint4*)(cur + rr * rowbytes + sc * CH * (int)sizeof(Tin));
+          if (!unal) {
+            const uint4* ep = (const uint4*)(cur + rr * rowbytes + sc * CH * (int)sizeof(Tin));
 #pragma unroll
-          for (int m = 0; m < (int)(CH * sizeof(Tin) / 16); ++m) u.q[m] = ep[m];
+            for (int m = 0; m < (int)(CH * sizeof(Tin) / 16); ++m) u.q[m] = ep[m];
+          } else {
+            const Tin* ee = (const Tin*)(cur + rr * rowbytes + mysh) + sc * CH;
+#pragma unroll
+            for (int m = 0; m < CH; ++m) u.e[m] = ee[m];
+          }
           int v[CH];
           int tot = 0;
 #pragma unroll
