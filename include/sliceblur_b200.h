@@ -107,8 +107,11 @@ const char* sb_last_error(void);
 int sb_check_kernel(const int64_t* radii, const double* weights, int k, int64_t extent);
 
 /* Bytes of device workspace sb_separable_filter_2d needs for this source
- * type and shape (0 when the single fused kernel applies; the size of the
- * int32 intermediate when the radius needs the two-kernel path). */
+ * type and shape: 0 when the single fused kernel applies; otherwise the
+ * intermediate plane of the two-kernel path (int32, or int64 past
+ * 2 p_max + 1 > 2048; its row pitch is the width rounded up to four elements)
+ * plus the generic kernels' scratch rows when they run.  Always ask: which path
+ * runs depends on type, width, channels and radii (and the path policy). */
 size_t sb_separable_filter_2d_workspace_bytes(int src_dtype, int64_t batch, int64_t height, int64_t width,
                                               int channels, const int64_t* radii, int k);
 

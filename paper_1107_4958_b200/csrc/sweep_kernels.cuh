@@ -2641,6 +2641,10 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
         rowsh_s[ptid] = unal ? (int)((size_t)rp & 15) : 0;
       }
       named_bar_sync(1, 32 * NPROD);
+      uint32_t tx_band = 0;  // bytes one interior chunk brings in
+      for (int i = 0; i < nt; ++i) tx_band += (uint32_t)((rowsh_s[i] + CW * C * ES + 15) & ~15);
+      const int my_sh = ptid < nt ? rowsh_s[ptid] : 0;
+      const Tin* my_rp = ptid < nt ? rowp_s[ptid] : src;
       // Chunk gc (counted over the CTA's bands) lives in staging buffer gc % STG; its landing is
       // phase gc / STG of sfull[gc % STG].  Interior chunks: one bulk copy per image row, issued
       // by one thread (expect_tx + complete_tx).  Edge chunks (border columns replicated,
@@ -2655,14 +2659,13 @@ __global__ void __launch_bounds__(STREAM_THREADS, 2)
         const int buf = (int)((cin_ctr + (uint32_t)j) % STG);
         unsigned char* sbuf = stage + buf * ntmax * srb;
         if (interior(j)) {
-          if (ptid == 0) {
-            uint32_t tx = 0;
-            for (int i = 0; i < nt; ++i) tx += (uint32_t)((rowsh_s[i] + CW * C * ES + 15) & ~15);
-            mbar_expect_tx(&sfull[buf], tx);
-            for (int i = 0; i < nt; ++i)
-              bulk_g2s(sbuf + i * srb, (const unsigned char*)(rowp_s[i] + (long long)xq0 * C) - rowsh_s[i],
-                       (uint32_t)((rowsh_s[i] + CW * C * ES + 15) & ~15), &sfull[buf]);
-          }
+          // lane i of the first producer warp copies image row i (the copies issue in parallel;
+          // the expect_tx arrive is the phase's only pending arrival, so an early complete_tx
+          // cannot complete it)
+          if (ptid == 0) mbar_expect_tx(&sfull[buf], tx_band);
+          if (ptid < nt)
+            bulk_g2s(sbuf + ptid * srb, (const unsigned char*)(my_rp + (long long)xq0 * C) - my_sh,
+                     (uint32_t)((my_sh + CW * C * ES + 15) & ~15), &sfull[buf]);
         } else {
           for (int i = 0; i < nt; ++i) {
             const Tin* rp = rowp_s[i];
