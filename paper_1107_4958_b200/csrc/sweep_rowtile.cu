@@ -343,4 +343,7 @@ const void* sweep_ptr_rowtile(int k) {
   }
 }
 
+// the two-band uint8 fused sweep with 4-byte staging copies (sweep_kernels.cuh, A4), compiled here
+// to balance the translation units
+const void* sweep_ptr_fused5w(int k) { return fused5w_ptr_for<>(k); }
 }  // namespace sb

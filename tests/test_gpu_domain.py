@@ -354,3 +354,27 @@ def test_streaming_rows_column_segments(dtype, shape, k, sigma):
             ref = O.separable_filter_2d(img, kern.radii, kern.weights)
             res = got[n, :, :, c] if cl else got[n]
             assert float(np.abs(res - ref).max()) <= BAR
+
+
+# uint8 rows that are 4-byte but not 16-byte multiples (1000-pixel-wide images) take the two-band
+# fused sweep instantiated with 4-byte staging copies; rows that are not even 4-byte multiples
+# keep the element staging.
+@pytest.mark.parametrize("shape,k,sigma", [
+    ((5, 60, 1000), 3, 10.0),
+    ((3, 45, 332), 3, 4.0),
+    ((2, 70, 1001), 3, 8.0),     # element staging
+    ((1, 90, 2012), 4, 6.0),     # last strip ends in a partial word run
+], ids=["1000-wide", "332-wide", "1001-wide-elements", "2012-wide"])
+def test_u8_fused_word_staging(shape, k, sigma):
+    rng = np.random.default_rng(shape[2])
+    x = (rng.random(shape) * 255).astype(np.uint8)
+    kern = A.table_kernel(k, sigma)
+    assert kern.max_radius <= 31
+    xt = torch.from_numpy(x).cuda()
+    got = F.separable_filter_batch(xt, kern).cpu().numpy()
+    with nat.path_policy(nat.SB_PATH_GENERIC):
+        gen = F.separable_filter_batch(xt, kern).cpu().numpy()
+    np.testing.assert_array_equal(got, gen)
+    for n in range(shape[0]):
+        ref = O.separable_filter_2d(x[n], kern.radii, kern.weights)
+        assert float(np.abs(got[n] - ref).max()) <= BAR
